@@ -1,0 +1,189 @@
+/*
+ * prismdg_b200.h -- C ABI of the B200-native wedge/tet DG time-stepping path.
+ *
+ * The reference (prismdg, arXiv 1607.03399) is a C++ library; its hot path is
+ *   run_simulation -> step -> TimeStepper::step (LSERK45) -> compute_rhs
+ * (proj/src/solver.cpp:591-666, 583-589, 536-557, 362-377).  This header is the
+ * thin C layer the reference's own C++ host code would call instead of its
+ * OpenMP compute_rhs / serial update: plain pointers and sizes, no C++ or torch
+ * types, status codes instead of exceptions.  Every entry point names the
+ * reference interface it replaces.
+ *
+ * Status codes follow the reference's exception taxonomy and CLI exit codes
+ * (proj/include/prismdg/types.hpp:14-34, proj/tools/main.cpp:84-98).
+ * Calls on one pdg_ctx are stream-ordered and not thread-safe.  There is no CPU
+ * fallback: pdg_create fails with PDG_ERR_CUDA when no sm_100 device exists.
+ */
+#ifndef PRISMDG_B200_H
+#define PRISMDG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PDG_OK 0
+#define PDG_ERR_CONFIG 2    /* ConfigError    (types.hpp:15-18)  */
+#define PDG_ERR_NUMERICAL 3 /* NumericalError (types.hpp:26-30)  */
+#define PDG_ERR_MESH 4      /* MeshError      (types.hpp:20-24)  */
+#define PDG_ERR_CUDA 5      /* device / CUDA runtime failure       */
+#define PDG_ERR_ANALYSIS 6  /* AnalysisError  (types.hpp:32-34)  */
+
+#define PDG_FLUX_UPWIND 0 /* FluxMode::upwind  (solver.hpp:14) */
+#define PDG_FLUX_CENTRAL 1
+#define PDG_FLUX_CUSTOM 2
+
+#define PDG_MASS_EXACT 0  /* QuadratureMode::exact  (operators.hpp:17) */
+#define PDG_MASS_LUMPED 1 /* QuadratureMode::lumped                      */
+#define PDG_MASS_WADG 2   /* weight-adjusted inverse (north-star extension) */
+
+typedef struct pdg_mesh pdg_mesh; /* prismdg::HybridMesh      (mesh.hpp:22-41)   */
+typedef struct pdg_disc pdg_disc; /* prismdg::Discretization  (solver.hpp:29-59) */
+typedef struct pdg_ctx pdg_ctx;   /* device-resident discretization + state      */
+
+/* Thread-local message of the last failing call (exception what()). */
+const char* pdg_last_error(void);
+int pdg_abi_version(void);
+
+/* ---------------------------------------------------------------- meshes
+ * Generators of proj/include/prismdg/mesh.hpp:61-92; media are {rho, kappa}. */
+int pdg_mesh_structured_hybrid_box(int nx, int ny, int nz_wedge, int nz_tet,
+                                   const double wedge_media[2], const double tet_media[2],
+                                   pdg_mesh** out);                       /* mesh.hpp:70 */
+int pdg_mesh_unstructured_wedge_box(int n, double xy_jitter, double z_amplitude, uint64_t seed,
+                                    const double media[2], pdg_mesh** out); /* mesh.hpp:78 */
+int pdg_mesh_arnold_wedge_box(int n, double delta, const double media[2],
+                              pdg_mesh** out);                            /* mesh.hpp:92 */
+/* stack_layers (mesh.hpp:63-65): xy[nv][2], tris[ntri][3] (0-based),
+ * z_bottom/z_top[nlayers][nv], sublayers[nlayers], media[nlayers][2]. */
+int pdg_mesh_stack_layers(int nv, const double* xy, int ntri, const int* tris, int nlayers,
+                          const double* z_bottom, const double* z_top, const int* sublayers,
+                          const double* media, pdg_mesh** out);
+int pdg_mesh_perturb_vertically(const pdg_mesh* in, double amplitude, uint64_t seed,
+                                pdg_mesh** out);                          /* mesh.hpp:86 */
+/* family meshes of analysis.hpp:41-49 (0 structured, 1 unstructured, 2 arnold) */
+int pdg_mesh_family(int family, double h, uint64_t seed, double xy_jitter, double z_amplitude,
+                    double arnold_delta, pdg_mesh** out);                 /* analysis.cpp:110-124 */
+int pdg_mesh_spectra(uint64_t seed, double amplitude, pdg_mesh** out);   /* analysis.cpp:237-239 */
+int pdg_mesh_load(const char* path, pdg_mesh** out);                     /* mesh.hpp:117 */
+int pdg_mesh_save(const pdg_mesh* mesh, const char* path);               /* mesh.hpp:118 */
+/* counts[0..2] = vertices, wedges, tets */
+int pdg_mesh_counts(const pdg_mesh* mesh, int64_t counts[3]);
+/* any pointer may be NULL; sizes from pdg_mesh_counts (media per element) */
+int pdg_mesh_export(const pdg_mesh* mesh, double* vertices, int* wedges, int* tets,
+                    double* media);
+int pdg_mesh_volume(const pdg_mesh* mesh, double* volume);               /* mesh.hpp:123 */
+void pdg_mesh_free(pdg_mesh* mesh);
+
+/* ---------------------------------------------------------------- discretization */
+typedef struct {
+  int degree, nq, nt, np_wedge, np_tet;
+  int64_t num_wedges, num_tets, total_dofs, total_nodes, num_faces;
+  int num_perms, num_interior_pairs, num_boundary_faces;
+  int flux_mode, mass_mode;
+} pdg_disc_info;
+
+/* build_discretization (solver.hpp:61-63). threads = OpenMP threads for setup. */
+int pdg_disc_build(const pdg_mesh* mesh, int degree, int flux_mode, double tau_p, double tau_u,
+                   int mass_mode, int threads, pdg_disc** out);
+int pdg_disc_get_info(const pdg_disc* d, pdg_disc_info* info);
+/* Discretization::elem_offset (solver.hpp:44), num_elements+1 entries */
+int pdg_disc_elem_offset(const pdg_disc* d, int64_t* out);
+/* per element face in (element, face) order: neighbour element (-1 boundary),
+ * neighbour face, permutation id (Connectivity, mesh.hpp:94-107) */
+int pdg_disc_face_table(const pdg_disc* d, int* nbr, int* nbr_face, int* perm_id);
+int pdg_disc_perm(const pdg_disc* d, int perm_id, int* out, int* len);
+/* FaceData::my_nodes / nbr_nodes of (e, f) (solver.hpp:52-58); len = nfp */
+int pdg_disc_face_nodes(const pdg_disc* d, int64_t e, int f, int* my_nodes, int* nbr_nodes,
+                        int* len);
+/* FaceData::normal, tau_p, tau_u of every face */
+int pdg_disc_face_phys(const pdg_disc* d, double* normals, double* tau_p, double* tau_u);
+/* physical node coordinates node_x/y/z (solver.hpp:47-48), total_nodes x 3 */
+int pdg_disc_node_coords(const pdg_disc* d, double* xyz);
+/* make_initial_state (solver.hpp:98-99): kind 0 standing_wave(c,rho) params={c,rho},
+ * kind 1 gaussian_pulse params={width,cx,cy,cz}; u has total_dofs entries */
+int pdg_disc_initial_state(const pdg_disc* d, int kind, const double* params, double t0,
+                           double* u);
+int pdg_disc_estimate_dt(const pdg_disc* d, double cfl, double* dt);      /* solver.hpp:81 */
+/* l2_error against the standing-wave pressure (analysis.hpp:30-32) */
+int pdg_disc_l2_error(const pdg_disc* d, const double* u, double time, double* err);
+/* per-element operator export for tests: L^{tri,k} (nt*nt, [k*nt+i]=L(i,k)),
+ * quad lifts (3*nq*nt), wedge scalars {rx,ry,sx,sy,tzJ,j0,jr,js,jf_bottom,jf_top,
+ * jf_quad[6],volume,surface_area} (18) */
+int pdg_disc_wedge_ops(const pdg_disc* d, int64_t w, double* tri_lift, double* quad_lift,
+                       double* scalars);
+void pdg_disc_free(pdg_disc* d);
+
+/* ---------------------------------------------------------------- device path */
+#define PDG_CTX_NATIVE_ORDER 1 /* keep reference element order on device (no Morton) */
+#define PDG_CTX_TIMING 2       /* bracket every stage kernel with CUDA events      */
+
+/* Upload a discretization to `device`. Replaces the first use of the host
+ * Discretization by compute_rhs / TimeStepper (solver.cpp:362-377, 536-557). */
+int pdg_create(const pdg_disc* d, int device, int flags, pdg_ctx** out);
+void pdg_destroy(pdg_ctx* ctx);
+/* state in the reference layout (element-major [p|ux|uy|uz], node i*(N+1)+j);
+ * u may be pageable or pinned host memory, or device memory when on_device=1 */
+int pdg_set_state(pdg_ctx* ctx, const double* u, int on_device);
+int pdg_get_state(pdg_ctx* ctx, double* u, int on_device);
+/* compute_rhs(const Discretization&, const double* u, double* rhs)
+ * (solver.hpp:67): writes every entry of rhs, reference layout */
+int pdg_rhs(pdg_ctx* ctx, const double* u, double* rhs, int on_device);
+/* the four phase functions (solver.hpp:71-74) on the context state: volume
+ * writes, surface accumulates, neither scales media; result via pdg_get_rhs */
+int pdg_wedge_volume(pdg_ctx* ctx);
+int pdg_wedge_surface(pdg_ctx* ctx);
+int pdg_tet_volume(pdg_ctx* ctx);
+int pdg_tet_surface(pdg_ctx* ctx);
+int pdg_get_rhs(pdg_ctx* ctx, double* rhs, int on_device);
+/* nsteps LSERK45 steps of TimeStepper::step (solver.cpp:536-557) on the
+ * resident state; *t_inout += nsteps*dt.  Asynchronous on the context stream. */
+int pdg_step_lserk(pdg_ctx* ctx, double dt, int nsteps, double* t_inout);
+/* compute_energy (solver.hpp:78): deterministic device reduction */
+int pdg_energy(pdg_ctx* ctx, double* energy);
+/* watchdog scan (solver.cpp:647-655): first element (reference id) with a
+ * non-finite DOF, or -1 */
+int pdg_check_finite(pdg_ctx* ctx, int64_t* first_bad_elem);
+int pdg_synchronize(pdg_ctx* ctx);
+/* the cudaStream_t all work of this context is issued on */
+void* pdg_stream(pdg_ctx* ctx);
+/* with PDG_CTX_TIMING: per-kernel-family accumulated device time and launch
+ * counts since the last reset; names: "wedge_stage","tet_stage","other" */
+int pdg_kernel_times(pdg_ctx* ctx, double* wedge_ms, int64_t* wedge_launches, double* tet_ms,
+                     int64_t* tet_launches, int reset);
+/* algorithmic bytes moved per launch of the wedge / tet stage kernels */
+int pdg_stage_bytes(pdg_ctx* ctx, double* wedge_bytes, double* tet_bytes);
+/* number of device elements and the device element -> reference element map */
+int pdg_device_order(pdg_ctx* ctx, int64_t* dev_to_ref);
+
+/* ---------------------------------------------------------------- run driver */
+typedef struct {
+  double final_time;      /* RunOptions (solver.hpp:126-137) */
+  double cfl;
+  double fixed_dt;        /* > 0 overrides the estimate */
+  double energy_interval; /* 0: log every step */
+  int watchdog_every;
+  double blowup_factor;
+  int integrator;         /* 0 lserk4 */
+} pdg_run_options;
+
+typedef struct {
+  int steps;              /* RunResult (solver.hpp:139-146) */
+  double dt, final_time, initial_energy, final_energy, max_energy_increase;
+  int num_logged;
+} pdg_run_result;
+
+/* run_simulation (solver.hpp:148-149) on the device; u_inout/time_inout hold
+ * the SolutionState (reference layout, host).  energy_log (may be NULL) gets
+ * up to max_log (time, energy) pairs. */
+int pdg_run_simulation(pdg_ctx* ctx, double* u_inout, double* time_inout,
+                       const pdg_run_options* opts, pdg_run_result* result, double* energy_log,
+                       int max_log);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PRISMDG_B200_H */

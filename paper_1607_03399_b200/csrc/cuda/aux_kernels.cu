@@ -1,0 +1,233 @@
+// Layout conversion, energy and watchdog kernels.
+//  * layout: reference state (element-major, wedge node i*(N+1)+j, solver.hpp:27-28)
+//    <-> device state (Morton element order, wedge [field][j][i]).
+//  * energy: 1/2 sum_k (p^T M_k p / kappa + rho u^T M_k u), M_k = M1D (x) M^{tri,k}
+//    for wedges (lumped: diag(w) (x) M^{tri,k}), J Mhat for tets
+//    (compute_energy, proj/src/solver.cpp:402-435); deterministic two-pass sum.
+//  * check_finite: first reference element holding a non-finite DOF
+//    (run_simulation watchdog, proj/src/solver.cpp:647-655).
+#include <cuda_runtime.h>
+
+#include "pdg_device.cuh"
+
+namespace pdg {
+
+namespace {
+
+template <int N, bool TO_DEVICE>
+__global__ void layout_kernel(long long Kw, long long Kt, const int* __restrict__ dev_to_ref,
+                              const long long* __restrict__ ref_offset,
+                              const double* __restrict__ src, double* __restrict__ dst) {
+  constexpr int NQ = nq_of(N), NT = nt_of(N), NPW = npw_of(N), NPT = npt_of(N);
+  const long long wdofs = Kw * 4 * NPW;
+  const long long total = wdofs + Kt * 4 * NPT;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    long long d, ref_local;
+    if (idx < wdofs) {
+      d = idx / (4 * NPW);
+      const int off = (int)(idx - d * 4 * NPW);
+      const int fld = off / NPW, node = off - fld * NPW;
+      const int j = node / NT, i = node - j * NT;
+      ref_local = (long long)fld * NPW + i * NQ + j;
+    } else {
+      const long long t = (idx - wdofs) / (4 * NPT);
+      d = Kw + t;
+      ref_local = (idx - wdofs) - t * 4 * NPT; // tets keep node order
+    }
+    const long long ref = ref_offset[dev_to_ref[d]] + ref_local;
+    if (TO_DEVICE)
+      dst[idx] = src[ref];
+    else
+      dst[ref] = src[idx];
+  }
+}
+
+template <int N>
+__global__ void wedge_energy_kernel(const EnergyParams p, int elems_per_block) {
+  // thread (el, i); partial energy of each block written to partials[block]
+  constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npw_of(N), WG = wg_of(N);
+  extern __shared__ double smem[];
+  const int E = elems_per_block;
+  double* sU = smem;                // [E][4*NP]
+  double* red = sU + E * 4 * NP;    // [blockDim]
+  const long long e0 = (long long)blockIdx.x * E;
+  const int nel = (int)((p.Kw - e0) < E ? (p.Kw - e0) : E);
+  for (int idx = threadIdx.x; idx < nel * 4 * NP; idx += blockDim.x) sU[idx] = p.u[e0 * 4 * NP + idx];
+  __syncthreads();
+  const int el = threadIdx.x / NT, i = threadIdx.x - el * NT;
+  double acc = 0.0;
+  if (el < nel) {
+    const double* G = p.wgeo + (e0 + el) * WG;
+    const double j0 = G[w_jac(N)], jr = G[w_jac(N) + 1], js = G[w_jac(N) + 2];
+    const double ikap = 1.0 / G[W_KAPPA], rho = 1.0 / G[W_IRHO];
+    const double* U = sU + el * 4 * NP;
+    for (int fld = 0; fld < 4; ++fld) {
+      const double* v = U + fld * NP;
+      double vm[NQ];
+#pragma unroll
+      for (int l = 0; l < NQ; ++l) vm[l] = 0.0;
+      for (int k = 0; k < NT; ++k) {
+        const double m = j0 * p.Mtri[k * NT + i] + jr * p.Xr[k * NT + i] + js * p.Xs[k * NT + i];
+#pragma unroll
+        for (int l = 0; l < NQ; ++l) vm[l] += v[l * NT + k] * m;
+      }
+      double q = 0.0;
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) {
+        double mv;
+        if (p.lumped) {
+          mv = p.w1d[j] * vm[j];
+        } else {
+          mv = 0.0;
+#pragma unroll
+          for (int l = 0; l < NQ; ++l) mv += p.M1D[j * NQ + l] * vm[l];
+        }
+        q += v[j * NT + i] * mv;
+      }
+      acc += (fld == 0 ? ikap : rho) * q;
+    }
+    acc *= 0.5;
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  // fixed-order tree reduction (deterministic)
+  for (int s = 1; s < blockDim.x; s <<= 1) {
+    if ((threadIdx.x % (2 * s)) == 0 && threadIdx.x + s < blockDim.x) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) p.partials[blockIdx.x] = red[0];
+}
+
+template <int N>
+__global__ void tet_energy_kernel(const EnergyParams p, int block_offset) {
+  constexpr int NP = npt_of(N);
+  __shared__ double sv[4 * NP];
+  __shared__ double red[NP];
+  const long long t = blockIdx.x;
+  const double* u = p.u + p.tet_base + t * 4 * NP;
+  for (int idx = threadIdx.x; idx < 4 * NP; idx += blockDim.x) sv[idx] = u[idx];
+  __syncthreads();
+  const int n = threadIdx.x;
+  const double* G = p.tgeo + t * kTG;
+  const double J = G[T_J], ikap = 1.0 / G[T_KAPPA], rho = 1.0 / G[T_IRHO];
+  double acc = 0.0;
+  for (int fld = 0; fld < 4; ++fld) {
+    double mv = 0.0;
+    for (int k = 0; k < NP; ++k) mv += p.Mtet[n * NP + k] * sv[fld * NP + k];
+    acc += (fld == 0 ? ikap : rho) * sv[fld * NP + n] * (J * mv);
+  }
+  red[n] = 0.5 * acc;
+  __syncthreads();
+  for (int s = 1; s < NP; s <<= 1) {
+    if ((n % (2 * s)) == 0 && n + s < NP) red[n] += red[n + s];
+    __syncthreads();
+  }
+  if (n == 0) p.partials[block_offset + t] = red[0];
+}
+
+__global__ void reduce_sum_kernel(const double* __restrict__ in, int n, double* __restrict__ out) {
+  // single block, fixed order: strided partial sums then a tree
+  __shared__ double red[1024];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += in[i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+template <int N>
+__global__ void check_finite_kernel(long long Kw, long long Kt, const double* __restrict__ u,
+                                    const int* __restrict__ dev_to_ref,
+                                    unsigned long long* first_bad) {
+  constexpr int NPW = npw_of(N), NPT = npt_of(N);
+  const long long wdofs = Kw * 4 * NPW;
+  const long long total = wdofs + Kt * 4 * NPT;
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    if (!isfinite(u[idx])) {
+      const long long d = idx < wdofs ? idx / (4 * NPW) : Kw + (idx - wdofs) / (4 * NPT);
+      atomicMin(first_bad, (unsigned long long)dev_to_ref[d]);
+    }
+  }
+}
+
+int grid_for(long long total, int threads) {
+  long long b = (total + threads - 1) / threads;
+  if (b > 148 * 32) b = 148 * 32;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+} // namespace
+
+#define PDG_DISPATCH(N, CALL)      \
+  switch (N) {                     \
+    case 1: { constexpr int NN = 1; CALL; } break; \
+    case 2: { constexpr int NN = 2; CALL; } break; \
+    case 3: { constexpr int NN = 3; CALL; } break; \
+    case 4: { constexpr int NN = 4; CALL; } break; \
+    case 5: { constexpr int NN = 5; CALL; } break; \
+    case 6: { constexpr int NN = 6; CALL; } break; \
+    case 7: { constexpr int NN = 7; CALL; } break; \
+    case 8: { constexpr int NN = 8; CALL; } break; \
+    case 9: { constexpr int NN = 9; CALL; } break; \
+    default: return cudaErrorInvalidValue; \
+  }
+
+cudaError_t launch_to_device_layout(int N, long long Kw, long long Kt, const int* dev_to_ref,
+                                    const long long* ref_offset, const double* src, double* dst,
+                                    cudaStream_t s) {
+  const long long total = Kw * 4 * npw_of(N) + Kt * 4 * npt_of(N);
+  if (total == 0) return cudaSuccess;
+  PDG_DISPATCH(N, (layout_kernel<NN, true><<<grid_for(total, 256), 256, 0, s>>>(Kw, Kt, dev_to_ref, ref_offset, src, dst)));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_to_reference_layout(int N, long long Kw, long long Kt, const int* dev_to_ref,
+                                       const long long* ref_offset, const double* src, double* dst,
+                                       cudaStream_t s) {
+  const long long total = Kw * 4 * npw_of(N) + Kt * 4 * npt_of(N);
+  if (total == 0) return cudaSuccess;
+  PDG_DISPATCH(N, (layout_kernel<NN, false><<<grid_for(total, 256), 256, 0, s>>>(Kw, Kt, dev_to_ref, ref_offset, src, dst)));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_energy(int N, const EnergyParams& p, int* nblocks_out, cudaStream_t s) {
+  int wb = 0;
+  const int NT = nt_of(N);
+  const int E = (256 / NT) > 0 ? 256 / NT : 1;
+  if (p.Kw > 0) {
+    wb = (int)((p.Kw + E - 1) / E);
+    const size_t smem = ((size_t)E * 4 * npw_of(N) + (size_t)E * NT) * 8;
+    PDG_DISPATCH(N, ({
+      cudaFuncSetAttribute(wedge_energy_kernel<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      wedge_energy_kernel<NN><<<wb, E * NT, smem, s>>>(p, E);
+    }));
+  }
+  if (p.Kt > 0) {
+    PDG_DISPATCH(N, (tet_energy_kernel<NN><<<(unsigned)p.Kt, npt_of(NN), 0, s>>>(p, wb)));
+  }
+  *nblocks_out = wb + (int)p.Kt;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_sum(const double* in, int n, double* out, cudaStream_t s) {
+  reduce_sum_kernel<<<1, 1024, 0, s>>>(in, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_check_finite(int N, long long Kw, long long Kt, const double* u,
+                                const int* dev_to_ref, unsigned long long* first_bad,
+                                cudaStream_t s) {
+  const long long total = Kw * 4 * npw_of(N) + Kt * 4 * npt_of(N);
+  if (total == 0) return cudaSuccess;
+  PDG_DISPATCH(N, (check_finite_kernel<NN><<<grid_for(total, 256), 256, 0, s>>>(Kw, Kt, u, dev_to_ref, first_bad)));
+  return cudaGetLastError();
+}
+
+} // namespace pdg

@@ -1,0 +1,603 @@
+// Device context: upload of a host Discretization into the B200 layout and the
+// stream-ordered operations behind the C ABI.
+#include "context.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <numeric>
+#include <string>
+#include <tuple>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+using prismdg::DeviceError;
+
+namespace pdg {
+
+namespace {
+
+#define PDG_CK(x)                                                                              \
+  do {                                                                                         \
+    cudaError_t e_ = (x);                                                                      \
+    if (e_ != cudaSuccess)                                                                     \
+      throw DeviceError(std::string(#x) + " failed: " + cudaGetErrorString(e_));             \
+  } while (0)
+
+template <class T>
+T* dalloc(std::size_t n) {
+  T* p = nullptr;
+  PDG_CK(cudaMalloc(&p, std::max<std::size_t>(n, 1) * sizeof(T)));
+  return p;
+}
+
+template <class T>
+T* upload(const std::vector<T>& h) {
+  T* d = dalloc<T>(h.size());
+  if (!h.empty()) PDG_CK(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return d;
+}
+
+// copy per-element blocks of `per` values from src (reference order) to dst
+// (device order), through a pinned staging buffer in chunks
+template <class T>
+void upload_permuted(T* dst, const T* src, std::size_t per, const std::vector<long long>& order) {
+  const std::size_t ne = order.size();
+  if (ne == 0 || per == 0) return;
+  const std::size_t chunk = std::max<std::size_t>(1, (std::size_t(64) << 20) / (per * sizeof(T)));
+  T* pin = nullptr;
+  PDG_CK(cudaMallocHost(&pin, std::min(chunk, ne) * per * sizeof(T)));
+  for (std::size_t c0 = 0; c0 < ne; c0 += chunk) {
+    const std::size_t cn = std::min(chunk, ne - c0);
+#pragma omp parallel for schedule(static)
+    for (long long q = 0; q < (long long)cn; ++q)
+      std::memcpy(pin + q * per, src + (std::size_t)order[c0 + q] * per, per * sizeof(T));
+    PDG_CK(cudaMemcpy(dst + c0 * per, pin, cn * per * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  cudaFreeHost(pin);
+}
+
+std::uint64_t spread_bits(std::uint64_t x) {
+  x &= 0x1fffffULL;
+  x = (x | x << 32) & 0x1f00000000ffffULL;
+  x = (x | x << 16) & 0x1f0000ff0000ffULL;
+  x = (x | x << 8) & 0x100f00f00f00f00fULL;
+  x = (x | x << 4) & 0x10c30c30c30c30c3ULL;
+  x = (x | x << 2) & 0x1249249249249249ULL;
+  return x;
+}
+
+// Morton order of element centroids (wedges and tets separately)
+std::vector<long long> locality_order(const prismdg::HybridMesh& mesh, bool wedges, bool native) {
+  const long long n = wedges ? mesh.num_wedges() : mesh.num_tets();
+  const long long off = wedges ? 0 : mesh.num_wedges();
+  std::vector<long long> order(n);
+  std::iota(order.begin(), order.end(), off);
+  if (native || n < 2) return order;
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (const auto& v : mesh.vertices)
+    for (int d = 0; d < 3; ++d) {
+      lo[d] = std::min(lo[d], v[d]);
+      hi[d] = std::max(hi[d], v[d]);
+    }
+  std::vector<std::uint64_t> key(n);
+#pragma omp parallel for schedule(static)
+  for (long long q = 0; q < n; ++q) {
+    double c[3] = {0, 0, 0};
+    const int* ids = wedges ? mesh.wedges[q].data() : mesh.tets[q].data();
+    const int nv = wedges ? 6 : 4;
+    for (int a = 0; a < nv; ++a)
+      for (int d = 0; d < 3; ++d) c[d] += mesh.vertices[ids[a]][d] / nv;
+    std::uint64_t k = 0;
+    for (int d = 0; d < 3; ++d) {
+      const double span = hi[d] > lo[d] ? hi[d] - lo[d] : 1.0;
+      const double t = std::min(1.0, std::max(0.0, (c[d] - lo[d]) / span));
+      k |= spread_bits((std::uint64_t)(t * 2097151.0)) << d;
+    }
+    key[q] = k;
+  }
+  std::stable_sort(order.begin(), order.end(),
+                   [&](long long a, long long b) { return key[a - off] < key[b - off]; });
+  return order;
+}
+
+void check_device(int device) {
+  int count = 0;
+  cudaError_t err = cudaGetDeviceCount(&count);
+  if (err != cudaSuccess || count == 0)
+    throw DeviceError("no CUDA device available (prismdg_b200 has no CPU fallback): " +
+                      std::string(cudaGetErrorString(err)));
+  if (device < 0 || device >= count) throw DeviceError("device index out of range");
+  cudaDeviceProp prop;
+  PDG_CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    throw DeviceError(std::string("prismdg_b200 kernels are built for sm_100a; device is ") +
+                      prop.name + " (sm_" + std::to_string(prop.major) + std::to_string(prop.minor) + ")");
+}
+
+int dev_node_of(const prismdg::Discretization& d, bool wedge, int nref) {
+  if (!wedge) return nref;
+  const int i = nref / d.nq, j = nref - i * d.nq;
+  return j * d.nt + i;
+}
+
+void launch_checked(pdg_ctx* c, const StageParams& p, bool wedge) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (c->flags & 2) {
+    PDG_CK(cudaEventCreate(&a));
+    PDG_CK(cudaEventCreate(&b));
+    PDG_CK(cudaEventRecord(a, c->stream));
+  }
+  cudaError_t err = wedge ? launch_wedge_stage(c->N, p, c->stream) : launch_tet_stage(c->N, p, c->stream);
+  if (err != cudaSuccess) throw DeviceError(std::string("stage kernel launch failed: ") + cudaGetErrorString(err));
+  if (c->flags & 2) {
+    PDG_CK(cudaEventRecord(b, c->stream));
+    c->pending.push_back({a, b, wedge ? 0 : 1});
+  }
+}
+
+StageParams base_params(pdg_ctx* c) {
+  StageParams p{};
+  p.Kw = c->Kw;
+  p.Kt = c->Kt;
+  p.tet_base = c->tet_base;
+  p.wgeo = c->wgeo;
+  p.wconn = c->wconn;
+  p.Lt = c->Lt;
+  p.QL = c->QL;
+  p.tgeo = c->tgeo;
+  p.tconn = c->tconn;
+  p.DrT = c->DrT;
+  p.DsT = c->DsT;
+  p.Dt = c->Dt;
+  p.prof = c->prof;
+  p.wface_dev = c->wface_dev;
+  p.tDrT = c->tDrT;
+  p.tDsT = c->tDsT;
+  p.tDtT = c->tDtT;
+  p.tLiftT = c->tLiftT;
+  p.tface = c->tface;
+  p.nbr_nodes = c->nbr_nodes;
+  p.max_nfp = c->max_nfp;
+  return p;
+}
+
+// LSERK45 coefficients, Carpenter & Kennedy (proj/src/solver.cpp:511-523)
+const double kRK4A[5] = {0.0, -567301805773.0 / 1357537059087.0, -2404267990393.0 / 2016746695238.0,
+                         -3550918686646.0 / 2091501179385.0, -1275806237668.0 / 842570457699.0};
+const double kRK4B[5] = {1432997174477.0 / 9575080441755.0, 5161836677717.0 / 13612068292357.0,
+                         1720146321549.0 / 2090206949498.0, 3134564353537.0 / 4481467310338.0,
+                         2277821191437.0 / 14882151754819.0};
+
+} // namespace
+
+pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags) {
+  check_device(device);
+  PDG_CK(cudaSetDevice(device));
+  if (d.degree < 1 || d.degree > kMaxN) throw prismdg::ConfigError("degree out of range for device path");
+  auto* c = new pdg_ctx();
+  try {
+    c->disc = &d;
+    c->device = device;
+    c->flags = flags;
+    PDG_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->N = d.degree;
+    c->nq = d.nq;
+    c->nt = d.nt;
+    c->npw = d.np_wedge;
+    c->npt = d.np_tet;
+    c->fw = fw_of(c->N);
+    c->Kw = d.mesh.num_wedges();
+    c->Kt = d.mesh.num_tets();
+    c->total_dofs = (long long)d.total_dofs;
+    c->tet_base = c->Kw * 4 * c->npw;
+    c->mass_mode = d.mass_mode;
+    const int N = c->N, nq = c->nq, nt = c->nt, npw = c->npw, npt = c->npt;
+    const bool native = flags & 1;
+
+    // ---- element order ------------------------------------------------------
+    const auto word = locality_order(d.mesh, true, native);
+    const auto tord = locality_order(d.mesh, false, native);
+    c->dev_to_ref_host.resize(c->Kw + c->Kt);
+    std::copy(word.begin(), word.end(), c->dev_to_ref_host.begin());
+    std::copy(tord.begin(), tord.end(), c->dev_to_ref_host.begin() + c->Kw);
+    const long long K = c->Kw + c->Kt;
+    std::vector<int> ref_to_dev(K);
+    for (long long q = 0; q < K; ++q) ref_to_dev[c->dev_to_ref_host[q]] = (int)q;
+    {
+      std::vector<int> d2r(K);
+      for (long long q = 0; q < K; ++q) d2r[q] = (int)c->dev_to_ref_host[q];
+      c->dev_to_ref = upload(d2r);
+      std::vector<long long> offs(d.elem_offset.begin(), d.elem_offset.end());
+      c->ref_offset = upload(offs);
+    }
+
+    // ---- neighbour node maps (one per distinct (kind, face, perm)) ----------
+    std::map<std::tuple<int, int, int>, int> combo_id;
+    std::vector<std::vector<int>> combos;
+    c->max_nfp = std::max(nq * nq, nt);
+    auto combo_of = [&](int nbr_ref, int nbr_face, int perm_id) {
+      const bool nw = d.mesh.kind(nbr_ref) == prismdg::ElemKind::wedge;
+      const auto key = std::make_tuple(nw ? 0 : 1, nbr_face, perm_id);
+      auto it = combo_id.find(key);
+      if (it != combo_id.end()) return it->second;
+      const auto& lst = nw ? d.refs.wedge.face_nodes[nbr_face] : d.refs.tet.face_nodes[nbr_face];
+      const auto& perm = d.conn.perms[perm_id];
+      std::vector<int> row(c->max_nfp, 0);
+      for (std::size_t m = 0; m < perm.size(); ++m) row[m] = dev_node_of(d, nw, lst[perm[m]]);
+      const int id = (int)combos.size();
+      combos.push_back(row);
+      combo_id.emplace(key, id);
+      return id;
+    };
+
+    // ---- wedge records --------------------------------------------------------
+    const int WG = wg_of(N);
+    {
+      std::vector<double> geo((std::size_t)c->Kw * WG, 0.0);
+      std::vector<int> conn((std::size_t)c->Kw * 10, -1);
+      for (long long q = 0; q < c->Kw; ++q) {
+        const int r = (int)word[q];
+        const auto& g = d.wgeo[r];
+        double* G = geo.data() + q * WG;
+        G[W_RX] = g.rx;
+        G[W_RY] = g.ry;
+        G[W_SX] = g.sx;
+        G[W_SY] = g.sy;
+        G[W_TZJ] = g.tzJ;
+        G[W_JFB] = g.jf_bottom;
+        G[W_JFT] = g.jf_top;
+        G[W_KAPPA] = d.mesh.media[r].kappa;
+        G[W_IRHO] = 1.0 / d.mesh.media[r].rho;
+        for (int j = 0; j < nq; ++j) {
+          G[W_TXJ + j] = d.txJ[(std::size_t)r * nq + j];
+          G[w_tyj(N) + j] = d.tyJ[(std::size_t)r * nq + j];
+        }
+        for (int f = 0; f < 5; ++f) {
+          const auto& fp = d.fphys[d.conn.face_offset[r] + f];
+          for (int a = 0; a < 3; ++a) G[w_nrm(N) + 3 * f + a] = fp.normal[a];
+          G[w_taup(N) + f] = fp.tau_p;
+          G[w_tauu(N) + f] = fp.tau_u;
+          const auto& fc = d.conn.at(r, f);
+          conn[q * 10 + 2 * f] = fc.nbr >= 0 ? ref_to_dev[fc.nbr] : -1;
+          conn[q * 10 + 2 * f + 1] = fc.nbr >= 0 ? combo_of(fc.nbr, fc.nbr_face, fc.perm_id) : 0;
+        }
+        G[w_jac(N)] = g.j0;
+        G[w_jac(N) + 1] = g.jr;
+        G[w_jac(N) + 2] = g.js;
+        for (int e = 0; e < 3; ++e) {
+          G[w_jac(N) + 3 + 2 * e] = g.jf_quad[e][0];
+          G[w_jac(N) + 4 + 2 * e] = g.jf_quad[e][1];
+        }
+      }
+      c->wgeo = upload(geo);
+      c->wconn = upload(conn);
+      std::vector<long long> word0(word);
+      c->Lt = dalloc<double>((std::size_t)c->Kw * nt * nt);
+      upload_permuted(c->Lt, d.tri_lift.data(), (std::size_t)nt * nt, word0);
+      if (d.quad_lift.empty()) throw prismdg::ConfigError("device path needs the quad lifts");
+      c->QL = dalloc<double>((std::size_t)c->Kw * 3 * nq * nt);
+      upload_permuted(c->QL, d.quad_lift.data(), (std::size_t)3 * nq * nt, word0);
+    }
+
+    // ---- tet records ------------------------------------------------------------
+    {
+      std::vector<double> geo((std::size_t)c->Kt * kTG, 0.0);
+      std::vector<int> conn((std::size_t)c->Kt * 8, -1);
+      const int nw = d.mesh.num_wedges();
+      for (long long q = 0; q < c->Kt; ++q) {
+        const int r = (int)tord[q];
+        const auto& g = d.tgeo[r - nw];
+        double* G = geo.data() + q * kTG;
+        const double v[9] = {g.rx, g.ry, g.rz, g.sx, g.sy, g.sz, g.tx, g.ty, g.tz};
+        for (int a = 0; a < 9; ++a) G[a] = v[a];
+        for (int f = 0; f < 4; ++f) G[T_LS + f] = g.lift_scale[f];
+        G[T_KAPPA] = d.mesh.media[r].kappa;
+        G[T_IRHO] = 1.0 / d.mesh.media[r].rho;
+        G[T_J] = g.J;
+        for (int f = 0; f < 4; ++f) {
+          const auto& fp = d.fphys[d.conn.face_offset[r] + f];
+          for (int a = 0; a < 3; ++a) G[T_NRM + 3 * f + a] = fp.normal[a];
+          G[T_TAUP + f] = fp.tau_p;
+          G[T_TAUU + f] = fp.tau_u;
+          const auto& fc = d.conn.at(r, f);
+          conn[q * 8 + 2 * f] = fc.nbr >= 0 ? ref_to_dev[fc.nbr] : -1;
+          conn[q * 8 + 2 * f + 1] = fc.nbr >= 0 ? combo_of(fc.nbr, fc.nbr_face, fc.perm_id) : 0;
+        }
+      }
+      c->tgeo = upload(geo);
+      c->tconn = upload(conn);
+    }
+    {
+      std::vector<int> flat;
+      for (const auto& row : combos) flat.insert(flat.end(), row.begin(), row.end());
+      if (flat.empty()) flat.assign(c->max_nfp, 0);
+      c->nbr_nodes = upload(flat);
+    }
+
+    // ---- shared reference tables ---------------------------------------------
+    {
+      const auto& tri = d.refs.tri;
+      const auto& line = d.refs.line;
+      std::vector<double> DrT((std::size_t)nt * nt), DsT(DrT.size()), Mtri(DrT.size()), Xr(DrT.size()),
+          Xs(DrT.size());
+      for (int k = 0; k < nt; ++k)
+        for (int i = 0; i < nt; ++i) {
+          DrT[(std::size_t)k * nt + i] = tri.dr(i, k);
+          DsT[(std::size_t)k * nt + i] = tri.ds(i, k);
+          Mtri[(std::size_t)k * nt + i] = tri.mass(k, i);
+          Xr[(std::size_t)k * nt + i] = tri.moment_r(k, i);
+          Xs[(std::size_t)k * nt + i] = tri.moment_s(k, i);
+        }
+      std::vector<double> Dt((std::size_t)nq * nq), M1D(Dt.size()), prof(2 * nq), w1d(nq);
+      const bool lumped = d.qmode == prismdg::QuadratureMode::lumped;
+      for (int j = 0; j < nq; ++j) {
+        for (int l = 0; l < nq; ++l) {
+          Dt[j * nq + l] = line.diff(j, l);
+          M1D[j * nq + l] = line.mass(j, l);
+        }
+        prof[j] = lumped ? line.lumped_lift_bottom[j] : line.lift_bottom[j];
+        prof[nq + j] = lumped ? line.lumped_lift_top[j] : line.lift_top[j];
+        w1d[j] = line.weights[j];
+      }
+      std::vector<int> wface(c->fw);
+      int m = 0;
+      for (int f = 0; f < 5; ++f)
+        for (int id : d.refs.wedge.face_nodes[f]) wface[m++] = dev_node_of(d, true, id);
+      const auto& tet = d.refs.tet;
+      std::vector<double> tDrT((std::size_t)npt * npt), tDsT(tDrT.size()), tDtT(tDrT.size()),
+          Mtet(tDrT.size()), tLiftT((std::size_t)4 * nt * npt);
+      for (int k = 0; k < npt; ++k)
+        for (int n = 0; n < npt; ++n) {
+          tDrT[(std::size_t)k * npt + n] = tet.dr(n, k);
+          tDsT[(std::size_t)k * npt + n] = tet.ds(n, k);
+          tDtT[(std::size_t)k * npt + n] = tet.dt(n, k);
+          Mtet[(std::size_t)n * npt + k] = tet.mass(n, k);
+        }
+      for (int col = 0; col < 4 * nt; ++col)
+        for (int n = 0; n < npt; ++n) tLiftT[(std::size_t)col * npt + n] = tet.lift(n, col);
+      std::vector<int> tface(4 * nt);
+      for (int f = 0; f < 4; ++f)
+        for (int q = 0; q < nt; ++q) tface[f * nt + q] = tet.face_nodes[f][q];
+      c->DrT = upload(DrT);
+      c->DsT = upload(DsT);
+      c->Dt = upload(Dt);
+      c->prof = upload(prof);
+      c->wface_dev = upload(wface);
+      c->tDrT = upload(tDrT);
+      c->tDsT = upload(tDsT);
+      c->tDtT = upload(tDtT);
+      c->tLiftT = upload(tLiftT);
+      c->tface = upload(tface);
+      c->Mtri = upload(Mtri);
+      c->Xr = upload(Xr);
+      c->Xs = upload(Xs);
+      c->M1D = upload(M1D);
+      c->w1d = upload(w1d);
+      c->Mtet = upload(Mtet);
+    }
+
+    // ---- state buffers --------------------------------------------------------
+    const std::size_t nd = (std::size_t)c->total_dofs;
+    c->u[0] = dalloc<double>(nd);
+    c->u[1] = dalloc<double>(nd);
+    c->res = dalloc<double>(nd);
+    c->stage = dalloc<double>(nd);
+    PDG_CK(cudaMemsetAsync(c->u[0], 0, nd * 8, c->stream));
+    PDG_CK(cudaMemsetAsync(c->res, 0, nd * 8, c->stream));
+    c->scalar = dalloc<double>(1);
+    c->badflag = dalloc<unsigned long long>(1);
+
+    // ---- algorithmic bytes per launch --------
+    const double w8 = 8.0;
+    const double wb_state_first = w8 * 3 * 4 * npw;  // u_in, res write, u_out
+    const double wb_state_later = w8 * 4 * 4 * npw;  // + res read
+    const double wb_ops = w8 * ((double)nt * nt + 3.0 * nt * nq + (34 + 2 * nq)) + 40.0;
+    c->wedge_bytes_first = (double)c->Kw * (wb_state_first + wb_ops);
+    c->wedge_bytes_later = (double)c->Kw * (wb_state_later + wb_ops);
+    const double tb_ops = w8 * 35 + 32.0;
+    c->tet_bytes_first = (double)c->Kt * (w8 * 3 * 4 * npt + tb_ops);
+    c->tet_bytes_later = (double)c->Kt * (w8 * 4 * 4 * npt + tb_ops);
+    PDG_CK(cudaStreamSynchronize(c->stream));
+  } catch (...) {
+    destroy_context(c);
+    throw;
+  }
+  return c;
+}
+
+void destroy_context(pdg_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& pe : c->pending) {
+    cudaEventDestroy(pe.a);
+    cudaEventDestroy(pe.b);
+  }
+  void* ptrs[] = {c->u[0], c->u[1], c->res, c->rhs, c->stage, c->wgeo, c->wconn, c->Lt, c->QL,
+                  c->tgeo, c->tconn, c->DrT, c->DsT, c->Dt, c->prof, c->wface_dev, c->tDrT,
+                  c->tDsT, c->tDtT, c->tLiftT, c->tface, c->nbr_nodes, c->Mtri, c->Xr, c->Xs,
+                  c->M1D, c->w1d, c->Mtet, c->partials, c->scalar, c->badflag, c->dev_to_ref,
+                  c->ref_offset};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+void set_state(pdg_ctx* c, const double* u, bool on_device) {
+  PDG_CK(cudaSetDevice(c->device));
+  const std::size_t bytes = (std::size_t)c->total_dofs * 8;
+  const double* src = u;
+  if (!on_device) {
+    PDG_CK(cudaMemcpyAsync(c->stage, u, bytes, cudaMemcpyHostToDevice, c->stream));
+    src = c->stage;
+  }
+  PDG_CK(launch_to_device_layout(c->N, c->Kw, c->Kt, c->dev_to_ref, c->ref_offset, src, c->u[c->cur], c->stream));
+}
+
+void get_state(pdg_ctx* c, double* u, bool on_device) {
+  PDG_CK(cudaSetDevice(c->device));
+  const std::size_t bytes = (std::size_t)c->total_dofs * 8;
+  double* dst = on_device ? u : c->stage;
+  PDG_CK(launch_to_reference_layout(c->N, c->Kw, c->Kt, c->dev_to_ref, c->ref_offset, c->u[c->cur], dst, c->stream));
+  if (!on_device) PDG_CK(cudaMemcpyAsync(u, c->stage, bytes, cudaMemcpyDeviceToHost, c->stream));
+  PDG_CK(cudaStreamSynchronize(c->stream));
+}
+
+static void ensure_rhs(pdg_ctx* c) {
+  if (!c->rhs) c->rhs = dalloc<double>((std::size_t)c->total_dofs);
+}
+
+void run_phase(pdg_ctx* c, bool wedge, bool volume) {
+  PDG_CK(cudaSetDevice(c->device));
+  ensure_rhs(c);
+  StageParams p = base_params(c);
+  p.u_in = c->u[c->cur];
+  p.rhs_out = c->rhs;
+  p.mode = volume ? M_VOLUME : (M_SURFACE | M_ACCUM);
+  launch_checked(c, p, wedge);
+}
+
+void compute_rhs(pdg_ctx* c, const double* u, double* rhs, bool on_device) {
+  PDG_CK(cudaSetDevice(c->device));
+  ensure_rhs(c);
+  const std::size_t bytes = (std::size_t)c->total_dofs * 8;
+  const double* src = u;
+  if (!on_device) {
+    PDG_CK(cudaMemcpyAsync(c->stage, u, bytes, cudaMemcpyHostToDevice, c->stream));
+    src = c->stage;
+  }
+  double* tmp = c->u[1 - c->cur]; // ping-pong target is free between steps
+  PDG_CK(launch_to_device_layout(c->N, c->Kw, c->Kt, c->dev_to_ref, c->ref_offset, src, tmp, c->stream));
+  StageParams p = base_params(c);
+  p.u_in = tmp;
+  p.rhs_out = c->rhs;
+  p.mode = M_VOLUME | M_SURFACE | M_MEDIA;
+  launch_checked(c, p, true);
+  launch_checked(c, p, false);
+  double* dst = on_device ? rhs : c->stage;
+  PDG_CK(launch_to_reference_layout(c->N, c->Kw, c->Kt, c->dev_to_ref, c->ref_offset, c->rhs, dst, c->stream));
+  if (!on_device) PDG_CK(cudaMemcpyAsync(rhs, c->stage, bytes, cudaMemcpyDeviceToHost, c->stream));
+  PDG_CK(cudaStreamSynchronize(c->stream));
+}
+
+void get_rhs(pdg_ctx* c, double* rhs, bool on_device) {
+  PDG_CK(cudaSetDevice(c->device));
+  ensure_rhs(c);
+  const std::size_t bytes = (std::size_t)c->total_dofs * 8;
+  double* dst = on_device ? rhs : c->stage;
+  PDG_CK(launch_to_reference_layout(c->N, c->Kw, c->Kt, c->dev_to_ref, c->ref_offset, c->rhs, dst, c->stream));
+  if (!on_device) PDG_CK(cudaMemcpyAsync(rhs, c->stage, bytes, cudaMemcpyDeviceToHost, c->stream));
+  PDG_CK(cudaStreamSynchronize(c->stream));
+}
+
+void step_lserk(pdg_ctx* c, double dt, int nsteps) {
+  PDG_CK(cudaSetDevice(c->device));
+  StageParams p = base_params(c);
+  p.res = c->res;
+  p.dt = dt;
+  for (int n = 0; n < nsteps; ++n)
+    for (int s = 0; s < 5; ++s) {
+      p.u_in = c->u[c->cur];
+      p.u_out = c->u[1 - c->cur];
+      p.a = kRK4A[s];
+      p.b = kRK4B[s];
+      p.mode = M_VOLUME | M_SURFACE | M_MEDIA | M_LSERK | (s == 0 ? M_FIRST : 0);
+      launch_checked(c, p, true);
+      launch_checked(c, p, false);
+      if (s == 0) ++c->stage_launches_first; else ++c->stage_launches_later;
+      c->cur = 1 - c->cur;
+    }
+}
+
+double energy(pdg_ctx* c) {
+  PDG_CK(cudaSetDevice(c->device));
+  const int NT = c->nt;
+  const int E = (256 / NT) > 0 ? 256 / NT : 1;
+  const int need = (int)((c->Kw + E - 1) / E + c->Kt) + 1;
+  if (need > c->partials_cap) {
+    if (c->partials) cudaFree(c->partials);
+    c->partials = dalloc<double>(need);
+    c->partials_cap = need;
+  }
+  EnergyParams p{};
+  p.Kw = c->Kw;
+  p.Kt = c->Kt;
+  p.tet_base = c->tet_base;
+  p.u = c->u[c->cur];
+  p.wgeo = c->wgeo;
+  p.tgeo = c->tgeo;
+  p.Mtri = c->Mtri;
+  p.Xr = c->Xr;
+  p.Xs = c->Xs;
+  p.M1D = c->M1D;
+  p.w1d = c->w1d;
+  p.Mtet = c->Mtet;
+  p.lumped = c->mass_mode == prismdg::MassMode::lumped;
+  p.partials = c->partials;
+  int nb = 0;
+  PDG_CK(launch_energy(c->N, p, &nb, c->stream));
+  if (nb == 0) return 0.0;
+  PDG_CK(launch_reduce_sum(c->partials, nb, c->scalar, c->stream));
+  double e = 0.0;
+  PDG_CK(cudaMemcpyAsync(&e, c->scalar, 8, cudaMemcpyDeviceToHost, c->stream));
+  PDG_CK(cudaStreamSynchronize(c->stream));
+  return e;
+}
+
+long long check_finite(pdg_ctx* c) {
+  PDG_CK(cudaSetDevice(c->device));
+  const unsigned long long none = std::numeric_limits<unsigned long long>::max();
+  PDG_CK(cudaMemcpyAsync(c->badflag, &none, 8, cudaMemcpyHostToDevice, c->stream));
+  PDG_CK(launch_check_finite(c->N, c->Kw, c->Kt, c->u[c->cur], c->dev_to_ref, c->badflag, c->stream));
+  unsigned long long r = none;
+  PDG_CK(cudaMemcpyAsync(&r, c->badflag, 8, cudaMemcpyDeviceToHost, c->stream));
+  PDG_CK(cudaStreamSynchronize(c->stream));
+  return r == none ? -1 : (long long)r;
+}
+
+void synchronize(pdg_ctx* c) {
+  PDG_CK(cudaSetDevice(c->device));
+  PDG_CK(cudaStreamSynchronize(c->stream));
+  PDG_CK(cudaGetLastError());
+}
+
+void kernel_times(pdg_ctx* c, double* wms, long long* wl, double* tms, long long* tl, bool reset) {
+  PDG_CK(cudaStreamSynchronize(c->stream));
+  for (auto& pe : c->pending) {
+    float ms = 0.0f;
+    PDG_CK(cudaEventElapsedTime(&ms, pe.a, pe.b));
+    if (pe.family == 0) {
+      c->wedge_ms += ms;
+      ++c->wedge_launches;
+    } else {
+      c->tet_ms += ms;
+      ++c->tet_launches;
+    }
+    cudaEventDestroy(pe.a);
+    cudaEventDestroy(pe.b);
+  }
+  c->pending.clear();
+  *wms = c->wedge_ms;
+  *wl = c->wedge_launches;
+  *tms = c->tet_ms;
+  *tl = c->tet_launches;
+  if (reset) {
+    c->wedge_ms = c->tet_ms = 0.0;
+    c->wedge_launches = c->tet_launches = 0;
+    c->stage_launches_first = c->stage_launches_later = 0;
+  }
+}
+
+void stage_bytes(pdg_ctx* c, double* wb, double* tb) {
+  // average over the 5 stages of a step (stage 0 does not read res)
+  *wb = (c->wedge_bytes_first + 4.0 * c->wedge_bytes_later) / 5.0;
+  *tb = (c->tet_bytes_first + 4.0 * c->tet_bytes_later) / 5.0;
+}
+
+} // namespace pdg

@@ -1,0 +1,82 @@
+#pragma once
+// Device context behind the C ABI (pdg_ctx): owns every device buffer of one
+// discretization on one GPU and issues all work on one stream.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "pdg_device.cuh"
+#include "prismdg/discretization.hpp"
+
+struct pdg_ctx {
+  const prismdg::Discretization* disc = nullptr; // must outlive the context
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int flags = 0;
+  int N = 0, nq = 0, nt = 0, npw = 0, npt = 0, fw = 0;
+  long long Kw = 0, Kt = 0, total_dofs = 0, tet_base = 0;
+  prismdg::MassMode mass_mode = prismdg::MassMode::exact;
+
+  double* u[2] = {nullptr, nullptr};
+  int cur = 0;
+  double* res = nullptr;
+  double* rhs = nullptr;
+  double* stage = nullptr; // reference-layout staging buffer (total_dofs)
+
+  double* wgeo = nullptr;
+  int* wconn = nullptr;
+  double* Lt = nullptr;
+  double* QL = nullptr;
+  double* tgeo = nullptr;
+  int* tconn = nullptr;
+
+  double *DrT = nullptr, *DsT = nullptr, *Dt = nullptr, *prof = nullptr;
+  int* wface_dev = nullptr;
+  double *tDrT = nullptr, *tDsT = nullptr, *tDtT = nullptr, *tLiftT = nullptr;
+  int* tface = nullptr;
+  int* nbr_nodes = nullptr;
+  int max_nfp = 0;
+  double *Mtri = nullptr, *Xr = nullptr, *Xs = nullptr, *M1D = nullptr, *w1d = nullptr,
+         *Mtet = nullptr;
+  double* partials = nullptr;
+  int partials_cap = 0;
+  double* scalar = nullptr;
+  unsigned long long* badflag = nullptr;
+
+  int* dev_to_ref = nullptr;      // device element -> reference element
+  long long* ref_offset = nullptr; // reference elem_offset (K+1)
+  std::vector<long long> dev_to_ref_host;
+
+  // timing (PDG_CTX_TIMING)
+  struct Pending {
+    cudaEvent_t a, b;
+    int family; // 0 wedge, 1 tet
+  };
+  std::vector<Pending> pending;
+  double wedge_ms = 0.0, tet_ms = 0.0;
+  long long wedge_launches = 0, tet_launches = 0;
+
+  double wedge_bytes_first = 0.0, wedge_bytes_later = 0.0;
+  double tet_bytes_first = 0.0, tet_bytes_later = 0.0;
+  long long stage_launches_first = 0, stage_launches_later = 0;
+};
+
+namespace pdg {
+
+/// builds device buffers; throws prismdg::DeviceError on CUDA failures
+pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags);
+void destroy_context(pdg_ctx* c);
+void set_state(pdg_ctx* c, const double* u, bool on_device);
+void get_state(pdg_ctx* c, double* u, bool on_device);
+void compute_rhs(pdg_ctx* c, const double* u, double* rhs, bool on_device);
+void run_phase(pdg_ctx* c, bool wedge, bool volume);
+void get_rhs(pdg_ctx* c, double* rhs, bool on_device);
+void step_lserk(pdg_ctx* c, double dt, int nsteps);
+double energy(pdg_ctx* c);
+long long check_finite(pdg_ctx* c);
+void synchronize(pdg_ctx* c);
+void kernel_times(pdg_ctx* c, double* wms, long long* wl, double* tms, long long* tl, bool reset);
+void stage_bytes(pdg_ctx* c, double* wb, double* tb);
+
+} // namespace pdg

@@ -1,0 +1,119 @@
+#pragma once
+// Device-side data layout and kernel interfaces of the B200 wedge/tet DG path.
+//
+// HBM layout:
+//  * device element order: wedges [0,Kw) then tets [Kw,Kw+Kt); within a kind the
+//    order is a locality-preserving (Morton) permutation of the reference ids.
+//  * state blocks: wedge d at d*4*NPW doubles, [field][slice j][tri node i]
+//    (tri node fastest -> a slice or a triangular face trace is one contiguous
+//    run); tet d at Kw*4*NPW + (d-Kw)*4*NPT, [field][node].
+//  * per-wedge L^{tri,k} stored [k][i] (thread i reads row i of L coalesced),
+//    quad lifts [face][a][i], a geometry/media record of WG doubles and a
+//    connectivity record of 10 ints (5 x {neighbour device id, node-map id}).
+#include <cstdint>
+
+namespace pdg {
+
+constexpr int kMaxN = 9;
+
+__host__ __device__ constexpr int nq_of(int N) { return N + 1; }
+__host__ __device__ constexpr int nt_of(int N) { return (N + 1) * (N + 2) / 2; }
+__host__ __device__ constexpr int npw_of(int N) { return nq_of(N) * nt_of(N); }
+__host__ __device__ constexpr int npt_of(int N) { return (N + 1) * (N + 2) * (N + 3) / 6; }
+__host__ __device__ constexpr int fw_of(int N) { return 2 * nt_of(N) + 3 * nq_of(N) * nq_of(N); }
+/// doubles per wedge geometry record
+__host__ __device__ constexpr int wg_of(int N) { return 44 + 2 * nq_of(N); }
+constexpr int kTG = 36; // doubles per tet record
+
+// wedge record offsets
+enum WRec : int {
+  W_RX = 0, W_RY, W_SX, W_SY, W_TZJ, W_JFB, W_JFT, W_KAPPA, W_IRHO,
+  W_TXJ = 9 // then TYJ at 9+nq, normals at 9+2nq (15), taup (5), tauu (5), j0 jr js jfq[6], pad
+};
+__host__ __device__ constexpr int w_tyj(int N) { return 9 + nq_of(N); }
+__host__ __device__ constexpr int w_nrm(int N) { return 9 + 2 * nq_of(N); }
+__host__ __device__ constexpr int w_taup(int N) { return 24 + 2 * nq_of(N); }
+__host__ __device__ constexpr int w_tauu(int N) { return 29 + 2 * nq_of(N); }
+__host__ __device__ constexpr int w_jac(int N) { return 34 + 2 * nq_of(N); } // j0 jr js jfq[6]
+
+// tet record offsets
+enum TRec : int {
+  T_RX = 0, T_RY, T_RZ, T_SX, T_SY, T_SZ, T_TX, T_TY, T_TZ, T_LS = 9, T_KAPPA = 13, T_IRHO = 14,
+  T_NRM = 15, T_TAUP = 27, T_TAUU = 31, T_J = 35
+};
+
+// stage kernel mode flags
+enum : int {
+  M_VOLUME = 1,    // volume terms
+  M_SURFACE = 2,   // surface terms
+  M_MEDIA = 4,     // scale by kappa, 1/rho
+  M_ACCUM = 8,     // rhs_out += (phase API) instead of =
+  M_LSERK = 16,    // fused LSERK45 stage update instead of writing rhs
+  M_FIRST = 32,    // a == 0: do not read res
+};
+
+struct StageParams {
+  long long Kw, Kt;
+  long long tet_base; // dof offset of the first tet block
+  const double* __restrict__ u_in;
+  double* __restrict__ u_out;
+  double* __restrict__ res;
+  double* __restrict__ rhs_out;
+  double a, b, dt;
+  int mode;
+  // wedges
+  const double* __restrict__ wgeo;
+  const int* __restrict__ wconn;
+  const double* __restrict__ Lt;
+  const double* __restrict__ QL;
+  // tets
+  const double* __restrict__ tgeo;
+  const int* __restrict__ tconn;
+  // shared reference tables
+  const double* __restrict__ DrT;  // [k][i]
+  const double* __restrict__ DsT;
+  const double* __restrict__ Dt;   // [j][l]
+  const double* __restrict__ prof; // [2][nq] tri-face lift profiles
+  const int* __restrict__ wface_dev; // [FW] device-layout node of each wedge face node
+  const double* __restrict__ tDrT; // [k][n]
+  const double* __restrict__ tDsT;
+  const double* __restrict__ tDtT;
+  const double* __restrict__ tLiftT; // [4*nt][n]
+  const int* __restrict__ tface; // [4*nt] tet face nodes
+  const int* __restrict__ nbr_nodes; // [combo][max_nfp]
+  int max_nfp;
+};
+
+struct EnergyParams {
+  long long Kw, Kt, tet_base;
+  const double* __restrict__ u;
+  const double* __restrict__ wgeo;
+  const double* __restrict__ tgeo;
+  const double* __restrict__ Mtri;  // [nt][nt]
+  const double* __restrict__ Xr;
+  const double* __restrict__ Xs;
+  const double* __restrict__ M1D;   // [nq][nq]
+  const double* __restrict__ w1d;   // GLL weights
+  const double* __restrict__ Mtet;  // [npt][npt]
+  int lumped;
+  double* __restrict__ partials;
+};
+
+// launchers (instantiated per degree in the .cu files)
+cudaError_t launch_wedge_stage(int N, const StageParams& p, cudaStream_t s);
+cudaError_t launch_tet_stage(int N, const StageParams& p, cudaStream_t s);
+int wedge_elems_per_block(int N);
+int tet_elems_per_block(int N);
+cudaError_t launch_energy(int N, const EnergyParams& p, int* nblocks_out, cudaStream_t s);
+cudaError_t launch_reduce_sum(const double* in, int n, double* out, cudaStream_t s);
+cudaError_t launch_to_device_layout(int N, long long Kw, long long Kt, const int* dev_to_ref,
+                                    const long long* ref_offset, const double* src_ref,
+                                    double* dst_dev, cudaStream_t s);
+cudaError_t launch_to_reference_layout(int N, long long Kw, long long Kt, const int* dev_to_ref,
+                                       const long long* ref_offset, const double* src_dev,
+                                       double* dst_ref, cudaStream_t s);
+cudaError_t launch_check_finite(int N, long long Kw, long long Kt, const double* u,
+                                const int* dev_to_ref, unsigned long long* first_bad,
+                                cudaStream_t s);
+
+} // namespace pdg
