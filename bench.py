@@ -1,0 +1,311 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 wedge/tet DG time-stepping path (BASELINE.json metric).
+
+Metric: DOF-updates/s = total_dofs x LSERK45 steps / device time (one step = 5
+fused stage launches).  Workload = BASELINE.json configs[1]: "order sweep
+N=1..7 on an extruded layered wedge mesh, ~1e6 elements per GPU" -- stack_layers
+on the structured n=100 surface (20,000 triangles) with three flat layers
+z=-1..-0.4 (15 sublayers), -0.4..0.2 (15), 0.2..1 (20): 1,000,000 wedges, media
+kappa = 1, 4, 2.25 and rho = 1, Gaussian pulse initial state,
+FP64, upwind flux, exact stored-lift mass.  The headline line is degree
+--degree (default 5); --degrees 1,2,...,7 adds the sweep under "sweep".
+
+Timing: W warm-up steps, then K steps bracketed by barrier + synchronize and
+CUDA events on the library's stream; value = total DOF-updates over all ranks
+/ max-over-ranks time.  Inputs (>= 0.1 GB state, 4 GB at N=5) are far larger
+than the 126 MB L2, so no flush is needed.  e2e = the same steps through the
+C ABI with host buffers: per step H2D of the state from pinned memory,
+pdg_step_lserk, D2H of the state.
+
+--impl reference: the reference's CPU algorithm (the oracle port in oracle/,
+because the reference itself cannot be built here) on the box's host cores,
+on a bounded sample (same surface, fewer sublayers).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "DOF-updates/sec (1/2/4/8 B200, N=1..7); per-kernel HBM GB/s vs roofline"
+UNIT = "DOF-updates/s"
+
+
+def layered_workload(surface_n, sublayers):
+    import paper_1607_03399_b200 as pdg
+    return pdg.layered_mesh(surface_n, [-1.0, -0.4, 0.2, 1.0], sublayers, [(1.0, 1.0), (1.0, 4.0), (1.0, 2.25)])
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            pk = json.load(fh)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_sample(degree, threads, target_s=15.0, parallel_update=False, surface_n=100, sublayers=(1, 1, 1)):
+    """Oracle (reference algorithm) DOF-updates/s on a bounded sample of the workload."""
+    import numpy as np
+    import oracle_binding as ob
+    import paper_1607_03399_b200 as pdg
+    mesh = layered_workload(surface_n, list(sublayers))
+    d = pdg.build_discretization(mesh, degree, threads=threads)
+    s = pdg.make_initial_state(d, "gaussian", [0.25, 0.0, 0.0, 0.0])
+    dt = pdg.estimate_dt(d, 0.5)
+    u = ob.lserk(d, s.u, dt, 1, threads, parallel_update)  # warm-up step
+    steps, elapsed = 0, 0.0
+    while elapsed < target_s and steps < 1000:
+        t0 = time.perf_counter()
+        u = ob.lserk(d, u, dt, 1, threads, parallel_update)
+        elapsed += time.perf_counter() - t0
+        steps += 1
+    rate = d.total_dofs * steps / elapsed
+    sample = (f"oracle port of solver.cpp:536-557 ({'parallel' if parallel_update else 'serial'} update), "
+              f"{mesh.num_wedges()} wedges (surface n={surface_n}, sublayers {list(sublayers)}), N={degree}, "
+              f"{steps} steps in {elapsed:.1f}s")
+    return rate, sample
+
+
+def run_reference_arm(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    rates = []
+    sample = ""
+    for it in range(args.warmup + args.steps):
+        rate, sample = cpu_sample(args.degree, threads, target_s=args.ref_seconds, parallel_update=False,
+                                  sublayers=(1, 1, 1))
+        if it >= args.warmup:
+            rates.append(rate)
+    value = sorted(rates)[len(rates) // 2] if rates else 0.0
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (gaussian pulse on generated layered wedge mesh)",
+        "config": {"workload": "configs[1] layered wedges, bounded CPU sample", "degree": args.degree},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def measure_degree(args, degree, ws, rank, local, peaks, with_e2e=True):
+    import numpy as np
+    import torch
+    import paper_1607_03399_b200 as pdg
+
+    t_setup = time.perf_counter()
+    mesh = layered_workload(args.surface_n, args.sublayers)
+    d = pdg.build_discretization(mesh, degree, threads=os.cpu_count() or 1)
+    s = pdg.make_initial_state(d, "gaussian", [0.25, 0.0, 0.0, 0.0])
+    dt = pdg.estimate_dt(d, 0.5)
+    ctx = pdg.DeviceContext(d, device=local, flags=pdg.capi.CTX_TIMING)
+    ctx.set_state(s.u)
+    setup_s = time.perf_counter() - t_setup
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
+
+    # warm-up
+    ctx.step(dt, args.warmup)
+    ctx.synchronize()
+    ctx.kernel_times(reset=True)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        ctx.step(dt, args.steps)
+        stop.record(stream)
+        stop.synchronize()
+    torch.cuda.synchronize()
+    ms = start.elapsed_time(stop)
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    kt = ctx.kernel_times(reset=True)
+    wbytes, tbytes = ctx.stage_bytes()
+    assert ctx.check_finite() == -1, "non-finite state after the timed steps"
+    dofs = d.total_dofs
+    value = dofs * args.steps * ws / (ms / 1e3)
+    wedge_avg_ms = kt["wedge_ms"] / max(1, kt["wedge_launches"])
+    achieved = wbytes / (wedge_avg_ms / 1e3) / 1e9
+    res = {
+        "degree": degree, "value": value, "ms_per_step": ms / args.steps, "total_dofs": dofs,
+        "wedges": mesh.num_wedges(), "setup_s": round(setup_s, 1),
+        "wedge_kernel_avg_ms": wedge_avg_ms, "wedge_stage_bytes": wbytes,
+        "wedge_kernel_share": kt["wedge_ms"] / ms if ms > 0 else None,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks[0], "unit": "GB/s",
+                     "frac": achieved / peaks[0], "traffic": None, "peak_source": peaks[1]},
+        "gpu_launches": int(kt["wedge_launches"] + kt["tet_launches"]),
+        "clocks": clk.summary(),
+    }
+    if with_e2e:
+        # e2e through the C ABI: pinned host state in, one step, state out, every step
+        host = torch.empty(dofs, dtype=torch.float64, pin_memory=True)
+        host.numpy()[:] = s.u
+        hptr = C.c_void_p(host.data_ptr())
+        lib = pdg.capi.lib()
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        torch.cuda.synchronize()
+        if ws > 1:
+            torch.distributed.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            pdg.capi.check(lib.pdg_set_state(ctx.handle, hptr, 0))
+            pdg.capi.check(lib.pdg_step_lserk(ctx.handle, dt, 1, None))
+            pdg.capi.check(lib.pdg_get_state(ctx.handle, hptr, 0))
+        el = time.perf_counter() - t0
+        if ws > 1:
+            t = torch.tensor([el], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            el = float(t.item())
+        res["e2e"] = {"value": dofs * e2e_steps * ws / el, "unit": UNIT, "h2d_bytes_per_step": dofs * 8,
+                      "d2h_bytes_per_step": dofs * 8, "steps": e2e_steps}
+    ctx.close()
+    del d, mesh
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--degree", type=int, default=5)
+    ap.add_argument("--degrees", default="", help="comma list for the order sweep, e.g. 1,2,3,4,5,6,7")
+    ap.add_argument("--surface-n", type=int, default=100)
+    ap.add_argument("--sublayers", default="15,15,20")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ref-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.sublayers = [int(x) for x in args.sublayers.split(",")]
+    args.warmup = max(3, args.warmup)
+
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    ws, rank, local = dist_env()
+    import torch
+    torch.cuda.set_device(local)
+    if ws > 1:
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks = load_peaks()
+    head = measure_degree(args, args.degree, ws, rank, local, peaks)
+    sweep = []
+    for deg in [int(x) for x in args.degrees.split(",") if x.strip()]:
+        if deg == args.degree:
+            continue
+        r = measure_degree(args, deg, ws, rank, local, peaks, with_e2e=False)
+        sweep.append({k: r[k] for k in ("degree", "value", "ms_per_step", "wedge_kernel_avg_ms", "roofline",
+                                        "total_dofs", "setup_s")})
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        rate, sample = cpu_sample(args.degree, threads, target_s=12.0, parallel_update=False, sublayers=(1, 1, 1))
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (gaussian pulse on generated layered wedge mesh, random-free)",
+            "config": {"workload": "configs[1]: layered wedge mesh, stack_layers n=100 surface x 50 sublayers "
+                                   "(1e6 wedges/GPU), exact stored-lift mass, upwind",
+                       "degree": args.degree, "wedges_per_gpu": head["wedges"], "total_dofs_per_gpu": head["total_dofs"],
+                       "parallelism": f"mesh partition x{ws}" if ws > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (state >> 126 MB), no flush"},
+            "roofline": head["roofline"], "cpu_baseline": cpu, "e2e": head.get("e2e"),
+            "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
+            "wedge_kernel_avg_ms": head["wedge_kernel_avg_ms"], "wedge_kernel_share": head["wedge_kernel_share"],
+            "setup_s": head["setup_s"],
+        }
+        if sweep:
+            line["sweep"] = sweep
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

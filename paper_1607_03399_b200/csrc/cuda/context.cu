@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -45,18 +46,23 @@ T* upload(const std::vector<T>& h) {
 // copy per-element blocks of `per` values from src (reference order) to dst
 // (device order), through a pinned staging buffer in chunks
 template <class T>
-void upload_permuted(T* dst, const T* src, std::size_t per, const std::vector<long long>& order) {
+void upload_permuted(T* dst, const T* src, std::size_t per, const std::vector<long long>& order,
+                     std::size_t dst_stride = 0, long long src_base = 0) {
+  // src rows of `per` values indexed by order[q] - src_base; dst rows of dst_stride (>= per, zero padded)
   const std::size_t ne = order.size();
+  if (dst_stride == 0) dst_stride = per;
   if (ne == 0 || per == 0) return;
-  const std::size_t chunk = std::max<std::size_t>(1, (std::size_t(64) << 20) / (per * sizeof(T)));
+  const std::size_t chunk = std::max<std::size_t>(1, (std::size_t(64) << 20) / (dst_stride * sizeof(T)));
   T* pin = nullptr;
-  PDG_CK(cudaMallocHost(&pin, std::min(chunk, ne) * per * sizeof(T)));
+  PDG_CK(cudaMallocHost(&pin, std::min(chunk, ne) * dst_stride * sizeof(T)));
   for (std::size_t c0 = 0; c0 < ne; c0 += chunk) {
     const std::size_t cn = std::min(chunk, ne - c0);
 #pragma omp parallel for schedule(static)
-    for (long long q = 0; q < (long long)cn; ++q)
-      std::memcpy(pin + q * per, src + (std::size_t)order[c0 + q] * per, per * sizeof(T));
-    PDG_CK(cudaMemcpy(dst + c0 * per, pin, cn * per * sizeof(T), cudaMemcpyHostToDevice));
+    for (long long q = 0; q < (long long)cn; ++q) {
+      std::memcpy(pin + q * dst_stride, src + (std::size_t)(order[c0 + q] - src_base) * per, per * sizeof(T));
+      if (dst_stride > per) std::memset(pin + q * dst_stride + per, 0, (dst_stride - per) * sizeof(T));
+    }
+    PDG_CK(cudaMemcpy(dst + c0 * dst_stride, pin, cn * dst_stride * sizeof(T), cudaMemcpyHostToDevice));
   }
   cudaFreeHost(pin);
 }
@@ -132,7 +138,9 @@ void launch_checked(pdg_ctx* c, const StageParams& p, bool wedge) {
     PDG_CK(cudaEventCreate(&b));
     PDG_CK(cudaEventRecord(a, c->stream));
   }
-  cudaError_t err = wedge ? launch_wedge_stage(c->N, p, c->stream) : launch_tet_stage(c->N, p, c->stream);
+  cudaError_t err = wedge ? (c->wedge_fma ? launch_wedge_stage_fma(c->N, p, c->stream)
+                                          : launch_wedge_stage(c->N, p, c->stream))
+                          : launch_tet_stage(c->N, p, c->stream);
   if (err != cudaSuccess) throw DeviceError(std::string("stage kernel launch failed: ") + cudaGetErrorString(err));
   if (c->flags & 2) {
     PDG_CK(cudaEventRecord(b, c->stream));
@@ -163,6 +171,7 @@ StageParams base_params(pdg_ctx* c) {
   p.tface = c->tface;
   p.nbr_nodes = c->nbr_nodes;
   p.max_nfp = c->max_nfp;
+  p.nbr_nodes_len = c->nbr_nodes_len;
   return p;
 }
 
@@ -182,6 +191,10 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags)
   auto* c = new pdg_ctx();
   try {
     c->disc = &d;
+    {
+      const char* kv = std::getenv("PDG_WEDGE_KERNEL");
+      c->wedge_fma = kv && std::string(kv) == "fma";
+    }
     c->device = device;
     c->flags = flags;
     PDG_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -239,7 +252,7 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags)
     const int WG = wg_of(N);
     {
       std::vector<double> geo((std::size_t)c->Kw * WG, 0.0);
-      std::vector<int> conn((std::size_t)c->Kw * 10, -1);
+      std::vector<int> conn((std::size_t)c->Kw * kWC, -1);
       for (long long q = 0; q < c->Kw; ++q) {
         const int r = (int)word[q];
         const auto& g = d.wgeo[r];
@@ -263,8 +276,8 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags)
           G[w_taup(N) + f] = fp.tau_p;
           G[w_tauu(N) + f] = fp.tau_u;
           const auto& fc = d.conn.at(r, f);
-          conn[q * 10 + 2 * f] = fc.nbr >= 0 ? ref_to_dev[fc.nbr] : -1;
-          conn[q * 10 + 2 * f + 1] = fc.nbr >= 0 ? combo_of(fc.nbr, fc.nbr_face, fc.perm_id) : 0;
+          conn[q * kWC + 2 * f] = fc.nbr >= 0 ? ref_to_dev[fc.nbr] : -1;
+          conn[q * kWC + 2 * f + 1] = fc.nbr >= 0 ? combo_of(fc.nbr, fc.nbr_face, fc.perm_id) : 0;
         }
         G[w_jac(N)] = g.j0;
         G[w_jac(N) + 1] = g.jr;
@@ -277,11 +290,11 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags)
       c->wgeo = upload(geo);
       c->wconn = upload(conn);
       std::vector<long long> word0(word);
-      c->Lt = dalloc<double>((std::size_t)c->Kw * nt * nt);
-      upload_permuted(c->Lt, d.tri_lift.data(), (std::size_t)nt * nt, word0);
-      if (d.quad_lift.empty()) throw prismdg::ConfigError("device path needs the quad lifts");
-      c->QL = dalloc<double>((std::size_t)c->Kw * 3 * nq * nt);
-      upload_permuted(c->QL, d.quad_lift.data(), (std::size_t)3 * nq * nt, word0);
+      c->Lt = dalloc<double>((std::size_t)c->Kw * lg_of(N));
+      upload_permuted(c->Lt, d.tri_lift.data(), (std::size_t)nt * nt, word0, lg_of(N));
+      if (c->Kw > 0 && d.quad_lift.empty()) throw prismdg::ConfigError("device path needs the quad lifts");
+      c->QL = dalloc<double>((std::size_t)c->Kw * qg_of(N));
+      upload_permuted(c->QL, d.quad_lift.data(), (std::size_t)3 * nq * nt, word0, qg_of(N));
     }
 
     // ---- tet records ------------------------------------------------------------
@@ -317,6 +330,7 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags)
       for (const auto& row : combos) flat.insert(flat.end(), row.begin(), row.end());
       if (flat.empty()) flat.assign(c->max_nfp, 0);
       c->nbr_nodes = upload(flat);
+      c->nbr_nodes_len = (int)flat.size();
     }
 
     // ---- shared reference tables ---------------------------------------------
@@ -396,7 +410,7 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags)
     const double w8 = 8.0;
     const double wb_state_first = w8 * 3 * 4 * npw;  // u_in, res write, u_out
     const double wb_state_later = w8 * 4 * 4 * npw;  // + res read
-    const double wb_ops = w8 * ((double)nt * nt + 3.0 * nt * nq + (34 + 2 * nq)) + 40.0;
+    const double wb_ops = w8 * ((double)nt * nt + 3.0 * nt * nq + (34 + 2 * nq)) + 4.0 * kWC;
     c->wedge_bytes_first = (double)c->Kw * (wb_state_first + wb_ops);
     c->wedge_bytes_later = (double)c->Kw * (wb_state_later + wb_ops);
     const double tb_ops = w8 * 35 + 32.0;

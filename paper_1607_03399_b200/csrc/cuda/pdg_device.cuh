@@ -8,8 +8,9 @@
 //    (tri node fastest -> a slice or a triangular face trace is one contiguous
 //    run); tet d at Kw*4*NPW + (d-Kw)*4*NPT, [field][node].
 //  * per-wedge L^{tri,k} stored [k][i] (thread i reads row i of L coalesced),
-//    quad lifts [face][a][i], a geometry/media record of WG doubles and a
-//    connectivity record of 10 ints (5 x {neighbour device id, node-map id}).
+//    quad lifts [face][a][i] (rows padded to lg_of / qg_of doubles), a
+//    geometry/media record of WG doubles and a connectivity record of kWC ints
+//    (5 x {neighbour device id, node-map id}, padded to 48 bytes).
 #include <cstdint>
 
 namespace pdg {
@@ -24,6 +25,12 @@ __host__ __device__ constexpr int fw_of(int N) { return 2 * nt_of(N) + 3 * nq_of
 /// doubles per wedge geometry record
 __host__ __device__ constexpr int wg_of(int N) { return 44 + 2 * nq_of(N); }
 constexpr int kTG = 36; // doubles per tet record
+constexpr int kWC = 12; // ints per wedge connectivity record (5 x {nbr, map} + pad, 48 B)
+__host__ __device__ constexpr int even_up(int x) { return (x + 1) & ~1; }
+/// global per-wedge strides (doubles) of L^{tri,k} and the quad lifts: rounded
+/// up to even so every element row is 16-byte aligned for bulk (TMA) copies
+__host__ __device__ constexpr int lg_of(int N) { return even_up(nt_of(N) * nt_of(N)); }
+__host__ __device__ constexpr int qg_of(int N) { return even_up(3 * npw_of(N)); }
 
 // wedge record offsets
 enum WRec : int {
@@ -82,6 +89,7 @@ struct StageParams {
   const int* __restrict__ tface; // [4*nt] tet face nodes
   const int* __restrict__ nbr_nodes; // [combo][max_nfp]
   int max_nfp;
+  int nbr_nodes_len; // ints in nbr_nodes
 };
 
 struct EnergyParams {
@@ -100,7 +108,9 @@ struct EnergyParams {
 };
 
 // launchers (instantiated per degree in the .cu files)
-cudaError_t launch_wedge_stage(int N, const StageParams& p, cudaStream_t s);
+cudaError_t launch_wedge_stage(int N, const StageParams& p, cudaStream_t s);      // FP64 tensor-core (DMMA) kernel
+cudaError_t launch_wedge_stage_fma(int N, const StageParams& p, cudaStream_t s);  // CUDA-core FMA kernel
+int wedge_elems_per_block_fma(int N);
 cudaError_t launch_tet_stage(int N, const StageParams& p, cudaStream_t s);
 int wedge_elems_per_block(int N);
 int tet_elems_per_block(int N);

@@ -1,0 +1,227 @@
+"""GPU parity tests: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Tolerances (FP64 everywhere; the GPU sums in a different order than the
+reference's Eigen products, so parity is by tolerance, not bitwise):
+  * single RHS evaluation: max-abs error <= 1e-12 x max|rhs| per field
+    (SURVEY.md 8(d) config 1 criterion), zero state -> exactly zero
+  * K time steps: relative L2 error of the state <= 1e-10 (FP64 criterion)
+  * energy: relative error <= 1e-12
+Meshes cover every face type: wedge-wedge (tri + quad), wedge-tet, tet-tet,
+reflective boundaries, perturbed (non-affine J) wedges, media jumps, lumped
+and central fluxes.
+"""
+import numpy as np
+import pytest
+
+import oracle_binding as ob
+import paper_1607_03399_b200 as pdg
+
+pytestmark = pytest.mark.gpu
+
+RHS_TOL = 1e-12
+STEP_TOL = 1e-10
+
+
+def field_errors(d, got, want):
+    """max-abs error / max-abs value for each of the 4 fields."""
+    off = d.elem_offset()
+    ne = d.num_elements()
+    errs = []
+    for f in range(4):
+        idx = np.concatenate([np.arange(off[e] + f * (off[e + 1] - off[e]) // 4,
+                                        off[e] + (f + 1) * (off[e + 1] - off[e]) // 4) for e in range(ne)])
+        scale = max(np.abs(want[idx]).max(), 1e-300)
+        errs.append(np.abs(got[idx] - want[idx]).max() / scale)
+    return errs
+
+
+def random_state(d, seed=1607):
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, d.total_dofs)
+
+
+MESHES = {
+    "wedge_box2": lambda: pdg.structured_wedge_box(2),
+    "hybrid_2211": lambda: pdg.structured_hybrid_box(2, 2, 1, 1, (1.0, 1.0), (1.0, 4.0)),
+    "tet_box": lambda: pdg.structured_hybrid_box(2, 2, 0, 2),
+    "unstructured_h05": lambda: pdg.make_family_mesh("unstructured", 0.5),
+    "spectra16": lambda: pdg.spectra_mesh(),
+    "layers_media": lambda: pdg.layered_mesh(3, [-1.0, -0.2, 1.0], [2, 3], [(1.0, 1.0), (2.0, 4.0)]),
+}
+
+
+@pytest.mark.parametrize("mesh_name", sorted(MESHES))
+@pytest.mark.parametrize("degree", [1, 2, 3, 4, 5])
+def test_rhs_matches_oracle(mesh_name, degree):
+    d = pdg.build_discretization(MESHES[mesh_name](), degree)
+    u = random_state(d)
+    want = ob.rhs(d, u)
+    got = pdg.compute_rhs(d, u)
+    errs = field_errors(d, got, want)
+    assert max(errs) <= RHS_TOL, errs
+
+
+@pytest.mark.parametrize("degree", [6, 7, 8, 9])
+def test_rhs_high_order(degree):
+    d = pdg.build_discretization(pdg.structured_hybrid_box(2, 2, 1, 1), degree)
+    u = random_state(d, seed=degree)
+    errs = field_errors(d, pdg.compute_rhs(d, u), ob.rhs(d, u))
+    assert max(errs) <= 10 * RHS_TOL, errs
+
+
+@pytest.mark.parametrize("flux,mass", [("central", "exact"), ("upwind", "lumped"), ("central", "lumped"),
+                                       ("custom", "exact")])
+def test_rhs_flux_and_mass_modes(flux, mass):
+    d = pdg.build_discretization(pdg.spectra_mesh(), 3, flux=flux, tau_p=0.7, tau_u=1.3, mass=mass)
+    u = random_state(d)
+    errs = field_errors(d, pdg.compute_rhs(d, u), ob.rhs(d, u))
+    assert max(errs) <= RHS_TOL, errs
+
+
+def test_zero_state_zero_rhs_exact():
+    d = pdg.build_discretization(pdg.structured_hybrid_box(2, 2, 1, 1), 3)
+    assert np.all(pdg.compute_rhs(d, np.zeros(d.total_dofs)) == 0.0)
+
+
+def test_rhs_deterministic_and_order_independent():
+    """Run to run bitwise; Morton vs native element order bitwise (per-element arithmetic is identical)."""
+    d = pdg.build_discretization(pdg.structured_hybrid_box(3, 3, 2, 1), 4)
+    u = random_state(d)
+    a = d.device(flags=0).rhs(u)
+    b = d.device(flags=0).rhs(u)
+    assert np.array_equal(a, b)
+    c = d.device(flags=pdg.capi.CTX_NATIVE_ORDER).rhs(u)
+    assert np.array_equal(a, c)
+
+
+@pytest.mark.parametrize("degree", [2, 4])
+def test_phase_functions(degree):
+    """volume writes, surface accumulates, no media scaling (solver.cpp:379-396)."""
+    d = pdg.build_discretization(pdg.structured_hybrid_box(2, 2, 1, 1, (2.0, 3.0), (1.0, 4.0)), degree)
+    u = random_state(d)
+    ctx = d.device()
+    for which, code in (("wedge", 0), ("tet", 2)):
+        ctx.set_state(u)
+        want = ob.phase(d, code, u, np.zeros(d.total_dofs))
+        want = ob.phase(d, code + 1, u, want)
+        ctx.phase(f"{which}_volume")
+        ctx.phase(f"{which}_surface")
+        got = ctx.get_rhs()
+        off = d.elem_offset()
+        nw = int(d.info.num_wedges)
+        rng = (slice(0, off[nw]) if which == "wedge" else slice(off[nw], off[-1]))
+        scale = np.abs(want[rng]).max()
+        assert np.abs(got[rng] - want[rng]).max() <= RHS_TOL * scale
+
+
+def test_state_roundtrip_bitwise():
+    d = pdg.build_discretization(pdg.structured_hybrid_box(2, 3, 2, 1), 5)
+    u = random_state(d)
+    ctx = d.device()
+    ctx.set_state(u)
+    assert np.array_equal(ctx.get_state(), u)
+
+
+def test_lserk_steps_match_oracle_config1():
+    """Config 1: unstructured h=0.5 wedge mesh, N=3, standing wave, fixed dt, 200 steps."""
+    d = pdg.build_discretization(pdg.make_family_mesh("unstructured", 0.5), 3)
+    s = pdg.make_initial_state(d)
+    dt = pdg.estimate_dt(d, 0.5)
+    ctx = d.device()
+    ctx.set_state(s.u)
+    ctx.step(dt, 200)
+    got = ctx.get_state()
+    want = ob.lserk(d, s.u, dt, 200)
+    rel = np.linalg.norm(got - want) / np.linalg.norm(want)
+    assert rel <= STEP_TOL, rel
+    assert abs(pdg.l2_error(d, got, 200 * dt) - pdg.l2_error(d, want, 200 * dt)) <= 1e-10 * pdg.l2_error(d, want, 200 * dt)
+
+
+def test_lserk_hybrid_random_state():
+    d = pdg.build_discretization(pdg.structured_hybrid_box(2, 2, 1, 1, (1.0, 1.0), (1.0, 4.0)), 4)
+    u = random_state(d)
+    dt = pdg.estimate_dt(d, 0.5)
+    ctx = d.device()
+    ctx.set_state(u)
+    ctx.step(dt, 20)
+    got = ctx.get_state()
+    want = ob.lserk(d, u, dt, 20)
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) <= STEP_TOL
+
+
+@pytest.mark.parametrize("mass", ["exact", "lumped"])
+def test_energy_matches_oracle(mass):
+    d = pdg.build_discretization(pdg.spectra_mesh(), 3, mass=mass)
+    u = random_state(d)
+    e_gpu = pdg.compute_energy(d, u)
+    e_orc = ob.energy(d, u)
+    assert abs(e_gpu - e_orc) <= 1e-12 * abs(e_orc)
+    h = pdg.build_discretization(pdg.structured_hybrid_box(2, 2, 1, 1), 2)
+    uh = random_state(h)
+    assert abs(pdg.compute_energy(h, uh) - ob.energy(h, uh)) <= 1e-12 * ob.energy(h, uh)
+
+
+def test_energy_closed_form():
+    """test_solver.cpp:146-162: p = 1, kappa = 1 -> E = half the volume = 4."""
+    d = pdg.build_discretization(pdg.structured_wedge_box(2), 2)
+    off = d.elem_offset()
+    u = np.zeros(d.total_dofs)
+    for e in range(d.num_elements()):
+        np_e = (off[e + 1] - off[e]) // 4
+        u[off[e]:off[e] + np_e] = 1.0
+    assert abs(pdg.compute_energy(d, u) - 4.0) <= 4e-12
+    assert pdg.compute_energy(d, np.zeros(d.total_dofs)) == 0.0
+
+
+def test_run_simulation_energy_decay_and_error():
+    """test_solver.cpp:146-162 / acceptance 4 on the GPU: upwind never gains energy."""
+    for mesh in (pdg.structured_wedge_box(2), pdg.structured_hybrid_box(2, 2, 1, 1), pdg.spectra_mesh()):
+        d = pdg.build_discretization(mesh, 3)
+        s = pdg.make_initial_state(d)
+        res = pdg.run_simulation(d, s, pdg.RunOptions(final_time=0.4))
+        assert res.max_energy_increase <= 1e-10 * res.initial_energy
+
+
+def test_watchdog_flags_nan():
+    d = pdg.build_discretization(pdg.structured_wedge_box(1), 1)
+    s = pdg.make_initial_state(d)
+    s.u[3] = np.nan
+    with pytest.raises(pdg.NumericalError):
+        pdg.run_simulation(d, s, pdg.RunOptions(final_time=1.0, watchdog_every=1))
+    ctx = d.device()
+    ctx.set_state(s.u)
+    assert ctx.check_finite() == 0
+
+
+def test_convergence_matches_paper_structured():
+    """Paper Table rates / Fig. errors through the GPU path (acceptance 1-2, h >= 0.25)."""
+    import json, os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_convergence.json")))
+    for N in (1, 2, 3):
+        errs = []
+        for k, h in enumerate([1.0, 0.5, 0.25]):
+            d = pdg.build_discretization(pdg.make_family_mesh("structured", h), N)
+            s = pdg.make_initial_state(d)
+            pdg.run_simulation(d, s, pdg.RunOptions(final_time=1.0, energy_interval=1.0))
+            e = pdg.l2_error(d, s.u, s.time)
+            ref = gold["structured_errors"][str(N)][k + 1]
+            assert abs(e - ref) <= 1e-2 * ref, (N, h, e, ref)
+            errs.append(e)
+        rate = pdg.fit_rate([1.0, 0.5, 0.25], errs)
+        assert abs(rate - gold["rates"]["structured"][N - 1]) <= 0.3
+
+
+def test_large_mesh_linearity_and_decay():
+    """Size-independent properties at ~100k wedges: rhs linearity and energy decay."""
+    m = pdg.layered_mesh(40, [-1.0, -0.4, 0.2, 1.0], [10, 10, 12], [(1.0, 1.0), (1.0, 4.0), (1.0, 2.25)])
+    d = pdg.build_discretization(m, 3)
+    ctx = d.device()
+    rng = np.random.default_rng(5)
+    u, v = rng.uniform(-1, 1, d.total_dofs), rng.uniform(-1, 1, d.total_dofs)
+    ru, rv, ruv = ctx.rhs(u), ctx.rhs(v), ctx.rhs(2.0 * u - 0.5 * v)
+    assert np.abs(ruv - (2.0 * ru - 0.5 * rv)).max() <= 1e-12 * np.abs(ruv).max() * 10
+    s = pdg.make_initial_state(d, "gaussian", [0.25, 0.0, 0.0, 0.0])
+    ctx.set_state(s.u)
+    e0 = ctx.energy()
+    ctx.step(pdg.estimate_dt(d, 0.5), 20)
+    assert ctx.energy() <= e0 * (1 + 1e-12)
+    assert ctx.check_finite() == -1
