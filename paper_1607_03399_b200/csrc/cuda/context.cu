@@ -138,9 +138,7 @@ void launch_checked(pdg_ctx* c, const StageParams& p, bool wedge) {
     PDG_CK(cudaEventCreate(&b));
     PDG_CK(cudaEventRecord(a, c->stream));
   }
-  cudaError_t err = wedge ? (c->wedge_fma ? launch_wedge_stage_fma(c->N, p, c->stream)
-                                          : launch_wedge_stage(c->N, p, c->stream))
-                          : launch_tet_stage(c->N, p, c->stream);
+  cudaError_t err = wedge ? launch_wedge_stage(c->N, p, c->stream) : launch_tet_stage(c->N, p, c->stream);
   if (err != cudaSuccess) throw DeviceError(std::string("stage kernel launch failed: ") + cudaGetErrorString(err));
   if (c->flags & 2) {
     PDG_CK(cudaEventRecord(b, c->stream));
@@ -182,6 +180,48 @@ const double kRK4B[5] = {1432997174477.0 / 9575080441755.0, 5161836677717.0 / 13
                          1720146321549.0 / 2090206949498.0, 3134564353537.0 / 4481467310338.0,
                          2277821191437.0 / 14882151754819.0};
 
+// L^{tri,k} and the quad lifts of every wedge, repacked into DMMA fragment
+// order (zero padded) and uploaded in device element order
+void upload_wedge_fragments(pdg_ctx* c, const prismdg::Discretization& d, const std::vector<long long>& order) {
+  const int N = c->N, nt = c->nt, nq = c->nq;
+  const int IT = it_of(N), KS = ks_of(N), KT = kt_of(N);
+  const std::size_t LF = lfrag_of(N), QF = qfrag_of(N);
+  const std::size_t ne = order.size();
+  const std::size_t chunk = std::max<std::size_t>(1, (std::size_t(64) << 20) / ((LF + QF) * 8));
+  double* pin = nullptr;
+  PDG_CK(cudaMallocHost(&pin, std::min(chunk, ne) * (LF + QF) * 8));
+  for (std::size_t c0 = 0; c0 < ne; c0 += chunk) {
+    const std::size_t cn = std::min(chunk, ne - c0);
+    double* pl = pin;
+    double* pq = pin + cn * LF;
+#pragma omp parallel for schedule(static)
+    for (long long q = 0; q < (long long)cn; ++q) {
+      const std::size_t r = (std::size_t)order[c0 + q];
+      const double* L = d.tri_lift.data() + r * nt * nt;        // [k*nt + i] = L(i,k)
+      const double* Q = d.quad_lift.data() + r * 3 * nq * nt;   // [(f*nq + a)*nt + i]
+      double* lf = pl + q * LF;
+      double* qf = pq + q * QF;
+      for (int t = 0; t < IT; ++t)
+        for (int lane = 0; lane < 32; ++lane) {
+          const int i = 8 * t + lane / 4, tg = lane % 4;
+          for (int s = 0; s < KS; ++s) {
+            const int k = 4 * s + tg;
+            lf[((std::size_t)t * KS + s) * 32 + lane] = (i < nt && k < nt) ? L[(std::size_t)k * nt + i] : 0.0;
+          }
+          for (int f = 0; f < 3; ++f)
+            for (int s = 0; s < KT; ++s) {
+              const int a = 4 * s + tg;
+              qf[(((std::size_t)t * 3 + f) * KT + s) * 32 + lane] =
+                  (i < nt && a < nq) ? Q[((std::size_t)f * nq + a) * nt + i] : 0.0;
+            }
+        }
+    }
+    PDG_CK(cudaMemcpy(c->Lt + c0 * LF, pl, cn * LF * 8, cudaMemcpyHostToDevice));
+    PDG_CK(cudaMemcpy(c->QL + c0 * QF, pq, cn * QF * 8, cudaMemcpyHostToDevice));
+  }
+  cudaFreeHost(pin);
+}
+
 } // namespace
 
 pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags) {
@@ -191,10 +231,6 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags)
   auto* c = new pdg_ctx();
   try {
     c->disc = &d;
-    {
-      const char* kv = std::getenv("PDG_WEDGE_KERNEL");
-      c->wedge_fma = kv && std::string(kv) == "fma";
-    }
     c->device = device;
     c->flags = flags;
     PDG_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -290,11 +326,10 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags)
       c->wgeo = upload(geo);
       c->wconn = upload(conn);
       std::vector<long long> word0(word);
-      c->Lt = dalloc<double>((std::size_t)c->Kw * lg_of(N));
-      upload_permuted(c->Lt, d.tri_lift.data(), (std::size_t)nt * nt, word0, lg_of(N));
       if (c->Kw > 0 && d.quad_lift.empty()) throw prismdg::ConfigError("device path needs the quad lifts");
-      c->QL = dalloc<double>((std::size_t)c->Kw * qg_of(N));
-      upload_permuted(c->QL, d.quad_lift.data(), (std::size_t)3 * nq * nt, word0, qg_of(N));
+      c->Lt = dalloc<double>((std::size_t)c->Kw * lfrag_of(N));
+      c->QL = dalloc<double>((std::size_t)c->Kw * qfrag_of(N));
+      upload_wedge_fragments(c, d, word0);
     }
 
     // ---- tet records ------------------------------------------------------------

@@ -14,7 +14,6 @@ struct pdg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   int flags = 0;
-  bool wedge_fma = false; // PDG_WEDGE_KERNEL=fma selects the CUDA-core kernel
   int N = 0, nq = 0, nt = 0, npw = 0, npt = 0, fw = 0;
   long long Kw = 0, Kt = 0, total_dofs = 0, tet_base = 0;
   prismdg::MassMode mass_mode = prismdg::MassMode::exact;

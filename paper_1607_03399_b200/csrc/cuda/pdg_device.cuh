@@ -8,7 +8,7 @@
 //    (tri node fastest -> a slice or a triangular face trace is one contiguous
 //    run); tet d at Kw*4*NPW + (d-Kw)*4*NPT, [field][node].
 //  * per-wedge L^{tri,k} stored [k][i] (thread i reads row i of L coalesced),
-//    quad lifts [face][a][i] (rows padded to lg_of / qg_of doubles), a
+//    quad lifts stored in DMMA-fragment-major order (lfrag_of / qfrag_of), a
 //    geometry/media record of WG doubles and a connectivity record of kWC ints
 //    (5 x {neighbour device id, node-map id}, padded to 48 bytes).
 #include <cstdint>
@@ -27,10 +27,16 @@ __host__ __device__ constexpr int wg_of(int N) { return 44 + 2 * nq_of(N); }
 constexpr int kTG = 36; // doubles per tet record
 constexpr int kWC = 12; // ints per wedge connectivity record (5 x {nbr, map} + pad, 48 B)
 __host__ __device__ constexpr int even_up(int x) { return (x + 1) & ~1; }
-/// global per-wedge strides (doubles) of L^{tri,k} and the quad lifts: rounded
-/// up to even so every element row is 16-byte aligned for bulk (TMA) copies
-__host__ __device__ constexpr int lg_of(int N) { return even_up(nt_of(N) * nt_of(N)); }
-__host__ __device__ constexpr int qg_of(int N) { return even_up(3 * npw_of(N)); }
+__host__ __device__ constexpr int ceil_div(int a, int b) { return (a + b - 1) / b; }
+// DMMA (m8n8k4) tiling of the per-wedge products: IT row tiles of 8 tri nodes,
+// KS k-steps of 4 over tri nodes, KT k-steps of 4 over slices
+__host__ __device__ constexpr int it_of(int N) { return ceil_div(nt_of(N), 8); }
+__host__ __device__ constexpr int ks_of(int N) { return ceil_div(nt_of(N), 4); }
+__host__ __device__ constexpr int kt_of(int N) { return ceil_div(nq_of(N), 4); }
+/// per-wedge L^{tri,k} in fragment-major order: [t][s][lane] = L(8t+lane/4, 4s+lane%4)
+__host__ __device__ constexpr int lfrag_of(int N) { return it_of(N) * ks_of(N) * 32; }
+/// per-wedge quad lifts: [t][face][s][lane] = QL_face(8t+lane/4, 4s+lane%4)
+__host__ __device__ constexpr int qfrag_of(int N) { return it_of(N) * 3 * kt_of(N) * 32; }
 
 // wedge record offsets
 enum WRec : int {
@@ -108,9 +114,7 @@ struct EnergyParams {
 };
 
 // launchers (instantiated per degree in the .cu files)
-cudaError_t launch_wedge_stage(int N, const StageParams& p, cudaStream_t s);      // FP64 tensor-core (DMMA) kernel
-cudaError_t launch_wedge_stage_fma(int N, const StageParams& p, cudaStream_t s);  // CUDA-core FMA kernel
-int wedge_elems_per_block_fma(int N);
+cudaError_t launch_wedge_stage(int N, const StageParams& p, cudaStream_t s); // FP64 tensor-core (DMMA) kernel
 cudaError_t launch_tet_stage(int N, const StageParams& p, cudaStream_t s);
 int wedge_elems_per_block(int N);
 int tet_elems_per_block(int N);

@@ -1,11 +1,11 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_gpu3.log 2>&1; echo "pytest exit $?"
-tail -25 gpurun_out/pytest_gpu3.log
-timeout 1500 python bench.py --steps 5 --warmup 3 --degree 5 --degrees 1,2,3,4,6,7 --no-cpu-baseline --e2e-steps 1 > gpurun_out/sweep_v3.json 2> gpurun_out/sweep_v3.err
+timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_gpu4.log 2>&1; echo "pytest exit $?"
+tail -25 gpurun_out/pytest_gpu4.log
+timeout 1500 python bench.py --steps 5 --warmup 3 --degree 5 --degrees 1,2,3,4,6,7 --no-cpu-baseline --e2e-steps 1 > gpurun_out/sweep_v4.json 2> gpurun_out/sweep_v4.err
 python - <<'PY'
 import json
-d=json.loads(open('gpurun_out/sweep_v3.json').read())
+d=json.loads(open('gpurun_out/sweep_v4.json').read())
 rows=[{'degree':d['config']['degree'],'value':d['value'],'roofline':d['roofline'],'wedge_kernel_avg_ms':d['wedge_kernel_avg_ms']}]+d.get('sweep',[])
 for r in sorted(rows,key=lambda r:r['degree']): print(r['degree'], f"{r['value']:.3e}", f"{r['wedge_kernel_avg_ms']:.3f} ms", f"{r['roofline']['achieved']:.0f} GB/s", f"{r['roofline']['frac']:.3f}")
 PY
-tail -5 gpurun_out/sweep_v3.err
+tail -5 gpurun_out/sweep_v4.err
