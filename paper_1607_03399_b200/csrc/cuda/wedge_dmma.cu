@@ -25,11 +25,13 @@
 //   TMA loads  (cp.async.bulk -> mbarrier): state, residual, L fragments, quad
 //              lift fragments, geometry/media record, connectivity record;
 //   gathers    neighbour face traces (LDG, L2-resident thanks to Morton order);
-//   TMA stores (cp.async.bulk global <- shared): updated state and residual.
+//   stores     updated state and residual straight from the DMMA fragments.
 // Each team double-buffers its stage so the next element's loads overlap.
 // Reference arithmetic: wedge_volume_elem / surface_elem / scale_media / lserk
 // (proj/src/solver.cpp:164-218, 258-335, 337-346, 541-551).
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "pdg_device.cuh"
 #include "tma.cuh"
@@ -49,8 +51,12 @@ __host__ __device__ constexpr int cf_stride(int x) {
 }
 
 constexpr int kComboCap = 4096; // ints of neighbour node maps kept in shared memory
+#ifndef PDG_WEDGE_STAGES
+#define PDG_WEDGE_STAGES 2
+#endif
+constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1 or 2)
 
-template <int N>
+template <int N, int NST_>
 struct DCfg {
   static constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npw_of(N), FW = fw_of(N), WG = wg_of(N);
   static constexpr int IT = it_of(N), KS = ks_of(N), KT = kt_of(N);
@@ -71,7 +77,7 @@ struct DCfg {
   static constexpr int TABLES = r2(2 * IT * KS * 32 + JT * KT * 32 + 2 * NQ + ceil_div(FW, 2) + kComboCap / 2);
   static constexpr int SMEM_BUDGET = 225 * 1024;
   // double-buffered stages unless even a single team would not fit
-  static constexpr int NSTAGE = (TABLES + 2 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET ? 2 : 1;
+  static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 2 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
   static constexpr int PER_TEAM = 2 + NSTAGE * STAGE + WORK;
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
   // <= 512 threads per CTA keeps >= 128 registers per thread
@@ -92,10 +98,10 @@ __device__ __forceinline__ void team_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <int N>
+template <int N, int NST>
 __device__ __forceinline__ void load_element(const StageParams& p, double* stg, long long e, const double* res_src,
                                              uint64_t* bar) {
-  using C = DCfg<N>;
+  using C = DCfg<N, NST>;
   constexpr int NP = C::NP;
   double* U = stg;
   double* R = U + C::USTR;
@@ -112,11 +118,12 @@ __device__ __forceinline__ void load_element(const StageParams& p, double* stg, 
   tma_load_1d(G + C::WG, p.wconn + e * kWC, 4 * kWC, bar);
 }
 
-template <int N, bool COMBO_SMEM>
-__global__ void __launch_bounds__(DCfg<N>::THREADS, 1) wedge_dmma_kernel(const StageParams p) {
-  using C = DCfg<N>;
+template <int N, bool COMBO_SMEM, bool FUSED, int NST>
+__global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(const StageParams p) {
+  using C = DCfg<N, NST>;
   constexpr int NQ = C::NQ, NT = C::NT, NP = C::NP, FW = C::FW, WG = C::WG, T = C::T;
   constexpr int KS = C::KS, JT = C::JT, JTL = C::JTL, KT = C::KT, VST = C::VST, TPB = C::TPB;
+  constexpr int QL_ = C::QF_LANE;
   extern __shared__ __align__(16) double smem[];
 
   // ---- shared reference tables (fragment-major, zero padded) ----------------
@@ -154,7 +161,7 @@ __global__ void __launch_bounds__(DCfg<N>::THREADS, 1) wedge_dmma_kernel(const S
   double* tbase = smem + C::TABLES + (size_t)team * C::PER_TEAM;
   uint64_t* bar = reinterpret_cast<uint64_t*>(tbase);
   double* stg0 = tbase + 2;
-  double* V = stg0 + C::NSTAGE * C::STAGE;
+  double* V = stg0 + NST * C::STAGE;
   double* Ftp = V + C::VS;      // tri-face fluxes: p part [2][NT]
   double* Ftu = Ftp + C::FTRI;  //                  u part
   double* Fqp = Ftu + C::FTRI;  // quad-face fluxes, fragment-major [f][jt][s][lane]
@@ -167,114 +174,122 @@ __global__ void __launch_bounds__(DCfg<N>::THREADS, 1) wedge_dmma_kernel(const S
   }
   __syncthreads();
 
+  // ---- per-thread face-node tasks, fixed for the whole kernel -----------------
+  int task_f[QL_], task_loc[QL_], task_my[QL_], task_pos[QL_];
+#pragma unroll
+  for (int q = 0; q < QL_; ++q) {
+    const int m = tt + 32 * T * q;
+    task_f[q] = -1;
+    if (m < FW) {
+      const int f = m < NT ? 0 : (m < 2 * NT ? 1 : 2 + (m - 2 * NT) / (NQ * NQ));
+      const int loc = m < 2 * NT ? m - f * NT : (m - 2 * NT) - (f - 2) * NQ * NQ;
+      task_f[q] = f;
+      task_loc[q] = loc;
+      task_my[q] = sWface[m];
+      if (f < 2) {
+        task_pos[q] = m;
+      } else {
+        const int a = loc / NQ, j = loc - a * NQ;
+        task_pos[q] = ((((f - 2) * JT + j / 8) * KT + a / 4) << 5) + ((j & 7) << 2) + (a & 3);
+      }
+    }
+  }
+
   const int mode = p.mode;
-  const bool vol = mode & M_VOLUME, surf = mode & M_SURFACE, lserk = mode & M_LSERK;
-  const bool first = mode & M_FIRST, accum = mode & M_ACCUM, media = mode & M_MEDIA;
+  const bool vol = FUSED || (mode & M_VOLUME), surf = FUSED || (mode & M_SURFACE);
+  const bool lserk = FUSED || (mode & M_LSERK), media = FUSED || (mode & M_MEDIA);
+  const bool first = mode & M_FIRST, accum = !FUSED && (mode & M_ACCUM);
   const double* res_src = lserk ? (first ? nullptr : p.res) : (accum ? p.rhs_out : nullptr);
   const long long total_teams = (long long)gridDim.x * TPB;
   long long e = (long long)blockIdx.x * TPB + team;
-  if (e < p.Kw && tt == 0) load_element<N>(p, stg0, e, res_src, bar);
+  if (e < p.Kw && tt == 0) load_element<N, NST>(p, stg0, e, res_src, bar);
 
   for (int n = 0; e < p.Kw; ++n) {
-    const int s = C::NSTAGE == 2 ? (n & 1) : 0;
+    const int s = NST == 2 ? (n & 1) : 0;
     const long long en = e + total_teams;
-    double* U = stg0 + s * C::STAGE;
-    double* R = U + C::USTR;
+    const double* U = stg0 + s * C::STAGE;
+    const double* R = U + C::USTR;
     const double* Lf = R + C::USTR;
     const double* Qf = Lf + C::LF;
     const double* G = Qf + C::QF;
     const int* Cn = reinterpret_cast<const int*>(G + WG);
-    if (C::NSTAGE == 2 && tt == 0 && en < p.Kw) {
-      bulk_wait_read<0>(); // the previous element's stores no longer read stage s^1
+    if (NST == 2 && tt == 0 && en < p.Kw) {
       fence_proxy_async_smem();
-      load_element<N>(p, stg0 + (s ^ 1) * C::STAGE, en, res_src, bar + (s ^ 1));
+      load_element<N, NST>(p, stg0 + (s ^ 1) * C::STAGE, en, res_src, bar + (s ^ 1));
     }
-    mbar_wait(bar + s, C::NSTAGE == 2 ? ((n >> 1) & 1) : (n & 1));
+    mbar_wait(bar + s, NST == 2 ? ((n >> 1) & 1) : (n & 1));
 
-    // ---- numerical fluxes on all face nodes (gathers batched per thread) -----
+    // ---- numerical fluxes on all face nodes -------------------------------------
     if (surf) {
+      double nb[QL_][4];
 #pragma unroll
-      for (int q0 = 0; q0 < C::QF_LANE; q0 += C::QB) {
-        double nb[C::QB][4];
-#pragma unroll
-        for (int qq = 0; qq < C::QB; ++qq) {
-          const int m = tt + 32 * T * (q0 + qq);
-          if (q0 + qq < C::QF_LANE && m < FW) {
-            const int f = m < NT ? 0 : (m < 2 * NT ? 1 : 2 + (m - 2 * NT) / (NQ * NQ));
-            const int loc = m < 2 * NT ? m - f * NT : (m - 2 * NT) - (f - 2) * NQ * NQ;
-            const int nbr = Cn[2 * f];
-            if (nbr >= 0) {
-              const int* combo = COMBO_SMEM ? sCombo : p.nbr_nodes;
-              const int node = COMBO_SMEM ? combo[Cn[2 * f + 1] * p.max_nfp + loc]
-                                          : __ldg(combo + Cn[2 * f + 1] * p.max_nfp + loc);
-              const double* src;
-              int fs;
-              if (nbr < p.Kw) {
-                src = p.u_in + (long long)nbr * 4 * NP + node;
-                fs = NP;
-              } else {
-                src = p.u_in + p.tet_base + (long long)(nbr - p.Kw) * 4 * npt_of(N) + node;
-                fs = npt_of(N);
-              }
-              nb[qq][0] = __ldg(src);
-              nb[qq][1] = __ldg(src + fs);
-              nb[qq][2] = __ldg(src + 2 * fs);
-              nb[qq][3] = __ldg(src + 3 * fs);
+      for (int q = 0; q < QL_; ++q) {
+        const int f = task_f[q];
+        if (f >= 0) {
+          const int nbr = Cn[2 * f];
+          if (nbr >= 0) {
+            const int mi = Cn[2 * f + 1] * p.max_nfp + task_loc[q];
+            const int node = COMBO_SMEM ? sCombo[mi] : __ldg(p.nbr_nodes + mi);
+            const double* src;
+            int fs;
+            if (nbr < p.Kw) {
+              src = p.u_in + (long long)nbr * 4 * NP + node;
+              fs = NP;
+            } else {
+              src = p.u_in + p.tet_base + (long long)(nbr - p.Kw) * 4 * npt_of(N) + node;
+              fs = npt_of(N);
             }
+            nb[q][0] = __ldg(src);
+            nb[q][1] = __ldg(src + fs);
+            nb[q][2] = __ldg(src + 2 * fs);
+            nb[q][3] = __ldg(src + 3 * fs);
           }
         }
+      }
 #pragma unroll
-        for (int qq = 0; qq < C::QB; ++qq) {
-          const int m = tt + 32 * T * (q0 + qq);
-          if (q0 + qq < C::QF_LANE && m < FW) {
-            const int f = m < NT ? 0 : (m < 2 * NT ? 1 : 2 + (m - 2 * NT) / (NQ * NQ));
-            const int my = sWface[m];
-            const double pm = U[my];
-            const double nx = G[w_nrm(N) + 3 * f], ny = G[w_nrm(N) + 3 * f + 1], nz = G[w_nrm(N) + 3 * f + 2];
-            const double taup = G[w_taup(N) + f], tauu = G[w_tauu(N) + f];
-            double fp, fu;
-            if (Cn[2 * f] >= 0) {
-              const double dp = nb[qq][0] - pm;
-              const double dux = nb[qq][1] - U[NP + my];
-              const double duy = nb[qq][2] - U[2 * NP + my];
-              const double duz = nb[qq][3] - U[3 * NP + my];
-              const double dun = nx * dux + ny * duy + nz * duz;
-              fp = 0.5 * (taup * dp - dun);
-              fu = 0.5 * (tauu * dun - dp);
-            } else {
-              const double dp = -2.0 * pm; // reflective: p+ = -p-, u+ = u-
-              fp = 0.5 * taup * dp;
-              fu = -0.5 * dp;
-            }
-            int pos;
-            if (m < 2 * NT) {
-              pos = m;
-              Ftp[pos] = fp;
-              Ftu[pos] = fu;
-            } else {
-              // quad face node (a, j): fragment position of B(k = a, n = j) of face f
-              const int loc = (m - 2 * NT) - (f - 2) * NQ * NQ;
-              const int a = loc / NQ, j = loc - a * NQ;
-              pos = ((((f - 2) * JT + j / 8) * KT + a / 4) << 5) + ((j & 7) << 2) + (a & 3);
-              Fqp[pos] = fp;
-              Fqu[pos] = fu;
-            }
+      for (int q = 0; q < QL_; ++q) {
+        const int f = task_f[q];
+        if (f >= 0) {
+          const int my = task_my[q];
+          const double pm = U[my];
+          const double nx = G[w_nrm(N) + 3 * f], ny = G[w_nrm(N) + 3 * f + 1], nz = G[w_nrm(N) + 3 * f + 2];
+          const double taup = G[w_taup(N) + f], tauu = G[w_tauu(N) + f];
+          double fp, fu;
+          if (Cn[2 * f] >= 0) {
+            const double dp = nb[q][0] - pm;
+            const double dun = nx * (nb[q][1] - U[NP + my]) + ny * (nb[q][2] - U[2 * NP + my]) +
+                               nz * (nb[q][3] - U[3 * NP + my]);
+            fp = 0.5 * (taup * dp - dun);
+            fu = 0.5 * (tauu * dun - dp);
+          } else {
+            const double dp = -2.0 * pm; // reflective: p+ = -p-, u+ = u-
+            fp = 0.5 * taup * dp;
+            fu = -0.5 * dp;
+          }
+          if (f < 2) {
+            Ftp[task_pos[q]] = fp;
+            Ftu[task_pos[q]] = fu;
+          } else {
+            Fqp[task_pos[q]] = fp;
+            Fqu[task_pos[q]] = fu;
           }
         }
       }
     }
+    team_sync(bar_id, 32 * T);
 
-    // ---- G1: vertical part of the pressure pre-lift buffer V[j][i] (tile w) --
+    // ---- G1: V[j][i] for row tile w, with the bottom/top pressure lifts folded in
     {
       const int i = 8 * w + gid;
-      if (vol) {
-        const double tzJ = G[W_TZJ];
+      const double tzJ = G[W_TZJ], jfb = G[W_JFB], jft = G[W_JFT];
+      const double fb = surf ? jfb * Ftp[i] : 0.0, ftop = surf ? jft * Ftp[NT + i] : 0.0;
 #pragma unroll
-        for (int jt = 0; jt < JT; ++jt) {
+      for (int jt = 0; jt < JT; ++jt) {
+        double d[2] = {0.0, 0.0};
+        if (vol) {
           const int jb = 8 * jt + gid;
           const int jc = jb < NQ ? jb : NQ - 1;
           const double sx_ = G[W_TXJ + jc], sy_ = G[w_tyj(N) + jc];
-          double d[2] = {0.0, 0.0};
 #pragma unroll
           for (int s2 = 0; s2 < KT; ++s2) {
             const int l = 4 * s2 + tig;
@@ -283,29 +298,12 @@ __global__ void __launch_bounds__(DCfg<N>::THREADS, 1) wedge_dmma_kernel(const S
             dmma(d, U[2 * NP + l * NT + i], sy_ * bd);
             dmma(d, U[3 * NP + l * NT + i], tzJ * bd);
           }
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const int j = 8 * jt + 2 * tig + c;
-            if (i < NT && j < NQ) V[j * VST + i] = -d[c];
-          }
         }
-      } else {
 #pragma unroll
-        for (int jt = 0; jt < JT; ++jt)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const int j = 8 * jt + 2 * tig + c;
-            if (i < NT && j < NQ) V[j * VST + i] = 0.0;
-          }
-      }
-    }
-    team_sync(bar_id, 32 * T);
-    // bottom / top pressure lifts share the L application of V
-    if (surf) {
-      const double jfb = G[W_JFB], jft = G[W_JFT];
-      for (int q = tt; q < NP; q += 32 * T) {
-        const int j = q / NT, i = q - j * NT;
-        V[j * VST + i] += jfb * sProf[j] * Ftp[i] + jft * sProf[NQ + j] * Ftp[NT + i];
+        for (int c = 0; c < 2; ++c) {
+          const int j = 8 * jt + 2 * tig + c;
+          if (i < NT && j < NQ) V[j * VST + i] = -d[c] + fb * sProf[j] + ftop * sProf[NQ + j];
+        }
       }
     }
     team_sync(bar_id, 32 * T);
@@ -321,10 +319,11 @@ __global__ void __launch_bounds__(DCfg<N>::THREADS, 1) wedge_dmma_kernel(const S
         const int nc = 8 * jt + gid;
         src[jt] = nc < NQ ? U + nc * NT : (nc == NQ ? Ftu : (nc == NQ + 1 ? Ftu + NT : Zero));
       }
-      double gx[JT][2], gy[JT][2], dv[JT][2], lv[JT][2], lp[JTL][2];
+      double gx[JT][2], gy[JT][2], dvx[JT][2], dvy[JT][2], lv[JT][2], lp[JTL][2];
 #pragma unroll
-      for (int jt = 0; jt < JT; ++jt) gx[jt][0] = gx[jt][1] = gy[jt][0] = gy[jt][1] = dv[jt][0] = dv[jt][1] =
-          lv[jt][0] = lv[jt][1] = 0.0;
+      for (int jt = 0; jt < JT; ++jt)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) gx[jt][c] = gy[jt][c] = dvx[jt][c] = dvy[jt][c] = lv[jt][c] = 0.0;
 #pragma unroll
       for (int jt = 0; jt < JTL; ++jt) lp[jt][0] = lp[jt][1] = 0.0;
 #pragma unroll
@@ -345,11 +344,10 @@ __global__ void __launch_bounds__(DCfg<N>::THREADS, 1) wedge_dmma_kernel(const S
           if (jt < JT) {
             const int jb = 8 * jt + gid;
             if (vol) {
-              const double bx = U[NP + jb * NT + k], by = U[2 * NP + jb * NT + k];
               dmma(gx[jt], cx, bp);
               dmma(gy[jt], cy, bp);
-              dmma(dv[jt], cx, bx);
-              dmma(dv[jt], cy, by);
+              dmma(dvx[jt], cx, U[NP + jb * NT + k]);
+              dmma(dvy[jt], cy, U[2 * NP + jb * NT + k]);
             }
             dmma(lv[jt], la, V[jb * VST + k]);
           }
@@ -377,8 +375,9 @@ __global__ void __launch_bounds__(DCfg<N>::THREADS, 1) wedge_dmma_kernel(const S
       // G5: quad-face lifts, one face at a time (uniform normal)
       double qp[JT][2], qx[JT][2], qy[JT][2], qz[JT][2];
 #pragma unroll
-      for (int jt = 0; jt < JT; ++jt) qp[jt][0] = qp[jt][1] = qx[jt][0] = qx[jt][1] = qy[jt][0] = qy[jt][1] =
-          qz[jt][0] = qz[jt][1] = 0.0;
+      for (int jt = 0; jt < JT; ++jt)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) qp[jt][c] = qx[jt][c] = qy[jt][c] = qz[jt][c] = 0.0;
       const double* nrm = G + w_nrm(N);
       if (surf) {
 #pragma unroll
@@ -399,9 +398,11 @@ __global__ void __launch_bounds__(DCfg<N>::THREADS, 1) wedge_dmma_kernel(const S
           }
         }
       }
-      // epilogue: rows i, columns j = 8 jt + 2 tig + c
+      // epilogue: rows i, columns j = 8 jt + 2 tig + c; results straight to HBM
       const double tzJ = G[W_TZJ], jfb = G[W_JFB], jft = G[W_JFT];
       const double kappa = G[W_KAPPA], irho = G[W_IRHO];
+      const double pa = p.a, pb = p.b, pdt = p.dt;
+      const long long ob = e * 4 * NP;
 #pragma unroll
       for (int jt = 0; jt < JT; ++jt)
 #pragma unroll
@@ -410,7 +411,7 @@ __global__ void __launch_bounds__(DCfg<N>::THREADS, 1) wedge_dmma_kernel(const S
           if (i < NT && j < NQ) {
             double rp = lv[jt][c], rux = 0.0, ruy = 0.0, ruz = 0.0;
             if (vol) {
-              rp -= dv[jt][c];
+              rp -= dvx[jt][c] + dvy[jt][c];
               rux = -(G[W_TXJ + j] * ly[jt][c] + gx[jt][c]);
               ruy = -(G[w_tyj(N) + j] * ly[jt][c] + gy[jt][c]);
               ruz = -(tzJ * ly[jt][c]);
@@ -432,64 +433,60 @@ __global__ void __launch_bounds__(DCfg<N>::THREADS, 1) wedge_dmma_kernel(const S
             const double rv[4] = {rp, rux, ruy, ruz};
 #pragma unroll
             for (int f = 0; f < 4; ++f) {
-              double& rr = R[f * NP + idx];
-              if (lserk)
-                rr = first ? p.dt * rv[f] : p.a * rr + p.dt * rv[f];
-              else
-                rr = accum ? rr + rv[f] : rv[f];
+              const int o = f * NP + idx;
+              if (lserk) {
+                const double rr = first ? pdt * rv[f] : pa * R[o] + pdt * rv[f];
+                p.res[ob + o] = rr;
+                p.u_out[ob + o] = U[o] + pb * rr;
+              } else {
+                p.rhs_out[ob + o] = accum ? R[o] + rv[f] : rv[f];
+              }
             }
           }
         }
     }
-    team_sync(bar_id, 32 * T);
-    if (lserk) {
-      const double b = p.b;
-      for (int q = tt; q < 4 * NP; q += 32 * T) U[q] += b * R[q];
-    }
-    team_sync(bar_id, 32 * T);
-    if (tt == 0) {
-      fence_proxy_async_smem();
-      if (lserk) {
-        tma_store_1d(p.u_out + e * 4 * NP, U, 32 * NP);
-        tma_store_1d(p.res + e * 4 * NP, R, 32 * NP);
-      } else {
-        tma_store_1d(p.rhs_out + e * 4 * NP, R, 32 * NP);
-      }
-      bulk_commit();
-      if (C::NSTAGE == 1 && en < p.Kw) { // single stage: reload once the stores have read it
-        bulk_wait_read<0>();
-        load_element<N>(p, stg0, en, res_src, bar);
-      }
-    }
+    team_sync(bar_id, 32 * T); // stage s and the work buffers are free again
+    if (NST == 1 && tt == 0 && en < p.Kw) load_element<N, NST>(p, stg0, en, res_src, bar);
     e = en;
   }
-  if (tt == 0) bulk_wait<0>();
 }
 
-template <int N, bool CS>
+template <int N, bool CS, bool FUSED, int NST>
 cudaError_t launch_dmma_NC(const StageParams& p, cudaStream_t s) {
-  using C = DCfg<N>;
+  using C = DCfg<N, NST>;
   static int grid_cap = 0;
+  auto kern = wedge_dmma_kernel<N, CS, FUSED, C::NSTAGE>;
   if (grid_cap == 0) {
-    cudaError_t err = cudaFuncSetAttribute(wedge_dmma_kernel<N, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)C::SMEM_BYTES);
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
     if (err != cudaSuccess) return err;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, wedge_dmma_kernel<N, CS>, C::THREADS, C::SMEM_BYTES);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM_BYTES);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
   if (p.Kw == 0) return cudaSuccess;
   const long long need = (p.Kw + C::TPB - 1) / C::TPB;
   const int grid = (int)(need < grid_cap ? need : grid_cap);
-  wedge_dmma_kernel<N, CS><<<grid, C::THREADS, C::SMEM_BYTES, s>>>(p);
+  kern<<<grid, C::THREADS, C::SMEM_BYTES, s>>>(p);
   return cudaGetLastError();
 }
 
 template <int N>
 cudaError_t launch_dmma_N(const StageParams& p, cudaStream_t s) {
-  return p.nbr_nodes_len <= kComboCap ? launch_dmma_NC<N, true>(p, s) : launch_dmma_NC<N, false>(p, s);
+  constexpr int F = M_VOLUME | M_SURFACE | M_MEDIA | M_LSERK;
+  const bool fused = (p.mode & F) == F && !(p.mode & M_ACCUM);
+  const bool cs = p.nbr_nodes_len <= kComboCap;
+  static const int stages = [] {
+    const char* v = std::getenv("PDG_WEDGE_STAGES");
+    return (v && v[0] == '1') ? 1 : kWedgeStages;
+  }();
+  if (stages == 1) {
+    if (fused) return cs ? launch_dmma_NC<N, true, true, 1>(p, s) : launch_dmma_NC<N, false, true, 1>(p, s);
+    return cs ? launch_dmma_NC<N, true, false, 1>(p, s) : launch_dmma_NC<N, false, false, 1>(p, s);
+  }
+  if (fused) return cs ? launch_dmma_NC<N, true, true, 2>(p, s) : launch_dmma_NC<N, false, true, 2>(p, s);
+  return cs ? launch_dmma_NC<N, true, false, 2>(p, s) : launch_dmma_NC<N, false, false, 2>(p, s);
 }
 
 } // namespace
@@ -506,7 +503,7 @@ cudaError_t launch_wedge_stage(int N, const StageParams& p, cudaStream_t s) {
 
 int wedge_elems_per_block(int N) {
   switch (N) {
-#define PDG_CASE(n) case n: return DCfg<n>::TPB;
+#define PDG_CASE(n) case n: return DCfg<n, kWedgeStages>::TPB;
     PDG_CASE(1) PDG_CASE(2) PDG_CASE(3) PDG_CASE(4) PDG_CASE(5) PDG_CASE(6) PDG_CASE(7)
     PDG_CASE(8) PDG_CASE(9)
 #undef PDG_CASE
