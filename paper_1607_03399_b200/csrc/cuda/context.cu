@@ -170,6 +170,8 @@ StageParams base_params(pdg_ctx* c) {
   p.nbr_nodes = c->nbr_nodes;
   p.max_nfp = c->max_nfp;
   p.nbr_nodes_len = c->nbr_nodes_len;
+  p.ticket = c->ticket;
+  p.ticket_host_next = &c->ticket_next;
   return p;
 }
 
@@ -440,6 +442,8 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags)
     PDG_CK(cudaMemsetAsync(c->res, 0, nd * 8, c->stream));
     c->scalar = dalloc<double>(1);
     c->badflag = dalloc<unsigned long long>(1);
+    c->ticket = dalloc<unsigned long long>(1);
+    PDG_CK(cudaMemset(c->ticket, 0, 8));
 
     // ---- algorithmic bytes per launch --------
     const double w8 = 8.0;
@@ -470,7 +474,7 @@ void destroy_context(pdg_ctx* c) {
   void* ptrs[] = {c->u[0], c->u[1], c->res, c->rhs, c->stage, c->wgeo, c->wconn, c->Lt, c->QL,
                   c->tgeo, c->tconn, c->DrT, c->DsT, c->Dt, c->prof, c->wface_dev, c->tDrT,
                   c->tDsT, c->tDtT, c->tLiftT, c->tface, c->nbr_nodes, c->Mtri, c->Xr, c->Xs,
-                  c->M1D, c->w1d, c->Mtet, c->partials, c->scalar, c->badflag, c->dev_to_ref,
+                  c->M1D, c->w1d, c->Mtet, c->partials, c->scalar, c->badflag, c->ticket, c->dev_to_ref,
                   c->ref_offset};
   for (void* p : ptrs)
     if (p) cudaFree(p);

@@ -44,6 +44,8 @@ struct pdg_ctx {
   int partials_cap = 0;
   double* scalar = nullptr;
   unsigned long long* badflag = nullptr;
+  unsigned long long* ticket = nullptr;       // device work counter (never reset)
+  unsigned long long ticket_next = 0;         // host copy of the next ticket base
 
   int* dev_to_ref = nullptr;      // device element -> reference element
   long long* ref_offset = nullptr; // reference elem_offset (K+1)

@@ -96,6 +96,10 @@ struct StageParams {
   const int* __restrict__ nbr_nodes; // [combo][max_nfp]
   int max_nfp;
   int nbr_nodes_len; // ints in nbr_nodes
+  // dynamic element scheduling: element = atomicAdd(ticket, 1) - ticket_base
+  unsigned long long* ticket;
+  unsigned long long ticket_base;
+  unsigned long long* ticket_host_next; // host side: next base (advanced by the launcher)
 };
 
 struct EnergyParams {

@@ -10,7 +10,7 @@
 //       dv    = (rx Dr + sx Ds) UX + (ry Dr + sy Ds) UY                (K = tri nodes)
 //   G3  [LP | L Fu_bottom | L Fu_top] = L [P | Fu0 | Fu1],  LV = L V     (K = tri nodes)
 //   G4  LY    = LP Dt^T   (Dt along slices; A fragments by quad shuffles)
-//   G5  [qp | qx | qy | qz] = sum_f QL_f [Fp_f ; n_c^f Fu_f]            (K = edge nodes)
+//   G5  qp = sum_f QL_f Fp_f,  qu_f = QL_f Fu_f (normals applied in the epilogue)
 // The metric is folded into the A fragments (rx Dr + sx Ds), the bottom/top
 // triangular-face pressure lifts are folded into V before G3, and
 // the epilogue adds the n-scaled velocity lifts, media scaling and the LSERK45
@@ -78,7 +78,7 @@ struct DCfg {
   static constexpr int SMEM_BUDGET = 225 * 1024;
   // double-buffered stages unless even a single team would not fit
   static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 2 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
-  static constexpr int PER_TEAM = 2 + NSTAGE * STAGE + WORK;
+  static constexpr int PER_TEAM = 4 + NSTAGE * STAGE + WORK;
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
   // <= 512 threads per CTA keeps >= 128 registers per thread
   static constexpr int TPB = cmax(1, cmin(cmin(15, 512 / (32 * T)), TPB_SMEM)); // teams per CTA
@@ -109,13 +109,16 @@ __device__ __forceinline__ void load_element(const StageParams& p, double* stg, 
   double* Q = L + C::LF;
   double* G = Q + C::QF;
   const uint32_t bytes = 8u * (4 * NP + C::LF + C::QF + C::WG) + 4u * kWC + (res_src ? 32u * NP : 0u);
+  // the state stays in L2 for the neighbours' trace gathers of this stage;
+  // everything else is touched once
+  const uint64_t keep = l2_policy_evict_last(), stream = l2_policy_evict_first();
   mbar_arrive_expect_tx(bar, bytes);
-  tma_load_1d(U, p.u_in + e * 4 * NP, 32 * NP, bar);
-  if (res_src) tma_load_1d(R, res_src + e * 4 * NP, 32 * NP, bar);
-  tma_load_1d(L, p.Lt + e * C::LF, 8 * C::LF, bar);
-  tma_load_1d(Q, p.QL + e * C::QF, 8 * C::QF, bar);
-  tma_load_1d(G, p.wgeo + e * C::WG, 8 * C::WG, bar);
-  tma_load_1d(G + C::WG, p.wconn + e * kWC, 4 * kWC, bar);
+  tma_load_1d_hint(U, p.u_in + e * 4 * NP, 32 * NP, bar, keep);
+  if (res_src) tma_load_1d_hint(R, res_src + e * 4 * NP, 32 * NP, bar, stream);
+  tma_load_1d_hint(L, p.Lt + e * C::LF, 8 * C::LF, bar, stream);
+  tma_load_1d_hint(Q, p.QL + e * C::QF, 8 * C::QF, bar, stream);
+  tma_load_1d_hint(G, p.wgeo + e * C::WG, 8 * C::WG, bar, stream);
+  tma_load_1d_hint(G + C::WG, p.wconn + e * kWC, 4 * kWC, bar, stream);
 }
 
 template <int N, bool COMBO_SMEM, bool FUSED, int NST>
@@ -160,7 +163,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
   const int bar_id = 1 + team;
   double* tbase = smem + C::TABLES + (size_t)team * C::PER_TEAM;
   uint64_t* bar = reinterpret_cast<uint64_t*>(tbase);
-  double* stg0 = tbase + 2;
+  double* stg0 = tbase + 4; // 2 mbarriers + 2 schedule slots
   double* V = stg0 + NST * C::STAGE;
   double* Ftp = V + C::VS;      // tri-face fluxes: p part [2][NT]
   double* Ftu = Ftp + C::FTRI;  //                  u part
@@ -200,13 +203,27 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
   const bool lserk = FUSED || (mode & M_LSERK), media = FUSED || (mode & M_MEDIA);
   const bool first = mode & M_FIRST, accum = !FUSED && (mode & M_ACCUM);
   const double* res_src = lserk ? (first ? nullptr : p.res) : (accum ? p.rhs_out : nullptr);
-  const long long total_teams = (long long)gridDim.x * TPB;
-  long long e = (long long)blockIdx.x * TPB + team;
-  if (e < p.Kw && tt == 0) load_element<N, NST>(p, stg0, e, res_src, bar);
+  // dynamic scheduling keeps all teams on a narrow, L2-resident window of the
+  // (Morton-ordered) element list, so neighbour traces hit in L2
+  volatile long long* slot = reinterpret_cast<volatile long long*>(bar + 2);
+  auto grab = [&]() -> long long {
+    return (long long)(atomicAdd(p.ticket, 1ULL) - p.ticket_base);
+  };
+  if (tt == 0) {
+    const long long e0 = grab();
+    slot[0] = e0;
+    if (e0 < p.Kw) load_element<N, NST>(p, stg0, e0, res_src, bar);
+  }
+  team_sync(bar_id, 32 * T);
+  long long e = slot[0];
 
   for (int n = 0; e < p.Kw; ++n) {
     const int s = NST == 2 ? (n & 1) : 0;
-    const long long en = e + total_teams;
+    long long en = 0;
+    if (tt == 0) {
+      en = grab();
+      slot[1] = en;
+    }
     const double* U = stg0 + s * C::STAGE;
     const double* R = U + C::USTR;
     const double* Lf = R + C::USTR;
@@ -372,37 +389,45 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
       constexpr int c0 = NQ % 8, c1 = (NQ + 1) % 8;
       const double lf0 = __shfl_sync(0xffffffffu, lp[NQ / 8][c0 & 1], gid * 4 + c0 / 2);
       const double lf1 = __shfl_sync(0xffffffffu, lp[(NQ + 1) / 8][c1 & 1], gid * 4 + c1 / 2);
-      // G5: quad-face lifts, one face at a time (uniform normal)
-      double qp[JT][2], qx[JT][2], qy[JT][2], qz[JT][2];
+      // G5: quad-face lifts; the velocity lift of each face is kept separately
+      // and scaled by that face's normal in the epilogue
+      double qp[JT][2], qu[3][JT][2];
 #pragma unroll
       for (int jt = 0; jt < JT; ++jt)
 #pragma unroll
-        for (int c = 0; c < 2; ++c) qp[jt][c] = qx[jt][c] = qy[jt][c] = qz[jt][c] = 0.0;
+        for (int c = 0; c < 2; ++c) qp[jt][c] = qu[0][jt][c] = qu[1][jt][c] = qu[2][jt][c] = 0.0;
       const double* nrm = G + w_nrm(N);
       if (surf) {
 #pragma unroll
-        for (int f = 0; f < 3; ++f) {
-          const double nx = nrm[6 + 3 * f], ny = nrm[7 + 3 * f], nz = nrm[8 + 3 * f];
+        for (int f = 0; f < 3; ++f)
 #pragma unroll
           for (int s2 = 0; s2 < KT; ++s2) {
             const double qa = Qf[(((t * 3 + f) * KT + s2) << 5) + lane];
 #pragma unroll
             for (int jt = 0; jt < JT; ++jt) {
               const int fo = (((f * JT + jt) * KT + s2) << 5) + lane;
-              const double bp = Fqp[fo], bu = Fqu[fo];
-              dmma(qp[jt], qa, bp);
-              dmma(qx[jt], qa, nx * bu);
-              dmma(qy[jt], qa, ny * bu);
-              dmma(qz[jt], qa, nz * bu);
+              dmma(qp[jt], qa, Fqp[fo]);
+              dmma(qu[f][jt], qa, Fqu[fo]);
             }
           }
-        }
       }
       // epilogue: rows i, columns j = 8 jt + 2 tig + c; results straight to HBM
       const double tzJ = G[W_TZJ], jfb = G[W_JFB], jft = G[W_JFT];
       const double kappa = G[W_KAPPA], irho = G[W_IRHO];
       const double pa = p.a, pb = p.b, pdt = p.dt;
-      const long long ob = e * 4 * NP;
+      double n_[5][3];
+#pragma unroll
+      for (int f = 0; f < 5; ++f)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) n_[f][a] = nrm[3 * f + a];
+      // per-lane base offset of position (i, j = 2 tig); (jt, c, field) add constants
+      const int lane_off = 2 * tig * NT + i;
+      const double* Ul = U + lane_off;
+      const double* Rl = R + lane_off;
+      const long long gofs = e * 4 * NP + lane_off;
+      double* resl = p.res + gofs;
+      double* uol = p.u_out + gofs;
+      double* rhsl = p.rhs_out + gofs;
 #pragma unroll
       for (int jt = 0; jt < JT; ++jt)
 #pragma unroll
@@ -418,10 +443,11 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
             }
             if (surf) {
               const double t0 = jfb * sProf[j] * lf0, t1 = jft * sProf[NQ + j] * lf1;
+              const double u2 = qu[0][jt][c], u3 = qu[1][jt][c], u4 = qu[2][jt][c];
               rp += qp[jt][c];
-              rux += nrm[0] * t0 + nrm[3] * t1 + qx[jt][c];
-              ruy += nrm[1] * t0 + nrm[4] * t1 + qy[jt][c];
-              ruz += nrm[2] * t0 + nrm[5] * t1 + qz[jt][c];
+              rux += n_[0][0] * t0 + n_[1][0] * t1 + n_[2][0] * u2 + n_[3][0] * u3 + n_[4][0] * u4;
+              ruy += n_[0][1] * t0 + n_[1][1] * t1 + n_[2][1] * u2 + n_[3][1] * u3 + n_[4][1] * u4;
+              ruz += n_[0][2] * t0 + n_[1][2] * t1 + n_[2][2] * u2 + n_[3][2] * u3 + n_[4][2] * u4;
             }
             if (media) {
               rp *= kappa;
@@ -429,17 +455,17 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
               ruy *= irho;
               ruz *= irho;
             }
-            const int idx = j * NT + i;
             const double rv[4] = {rp, rux, ruy, ruz};
+            constexpr int cst[2] = {0, NT};
 #pragma unroll
             for (int f = 0; f < 4; ++f) {
-              const int o = f * NP + idx;
+              const int o = f * NP + 8 * jt * NT + cst[c];
               if (lserk) {
-                const double rr = first ? pdt * rv[f] : pa * R[o] + pdt * rv[f];
-                p.res[ob + o] = rr;
-                p.u_out[ob + o] = U[o] + pb * rr;
+                const double rr = first ? pdt * rv[f] : pa * Rl[o] + pdt * rv[f];
+                __stcs(resl + o, rr); // streaming stores: evict first
+                __stcs(uol + o, Ul[o] + pb * rr);
               } else {
-                p.rhs_out[ob + o] = accum ? R[o] + rv[f] : rv[f];
+                __stcs(rhsl + o, accum ? Rl[o] + rv[f] : rv[f]);
               }
             }
           }
@@ -447,7 +473,8 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
     }
     team_sync(bar_id, 32 * T); // stage s and the work buffers are free again
     if (NST == 1 && tt == 0 && en < p.Kw) load_element<N, NST>(p, stg0, en, res_src, bar);
-    e = en;
+    e = slot[1];
+    team_sync(bar_id, 32 * T); // slot[1] is read by every thread before it is rewritten
   }
 }
 
@@ -468,7 +495,10 @@ cudaError_t launch_dmma_NC(const StageParams& p, cudaStream_t s) {
   if (p.Kw == 0) return cudaSuccess;
   const long long need = (p.Kw + C::TPB - 1) / C::TPB;
   const int grid = (int)(need < grid_cap ? need : grid_cap);
-  kern<<<grid, C::THREADS, C::SMEM_BYTES, s>>>(p);
+  StageParams q = p;
+  q.ticket_base = *p.ticket_host_next;
+  *p.ticket_host_next += (unsigned long long)p.Kw + (unsigned long long)grid * C::TPB;
+  kern<<<grid, C::THREADS, C::SMEM_BYTES, s>>>(q);
   return cudaGetLastError();
 }
 
