@@ -244,6 +244,55 @@ def measure_degree(args, degree, ws, rank, local, peaks, with_e2e=True):
     return res
 
 
+def measure_degree_dist(args, degree, ws, rank, local, peaks):
+    """N > 1: weak scaling, rank r owns the r-th slab of 1e6 wedges (stack of ws copies of
+    the config-2 slab, config 5); ghosts are one sublayer above and below and are
+    refreshed with NCCL point-to-point before every LSERK stage."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_1607_03399_b200 as pdg
+    from paper_1607_03399_b200 import partition as P
+    from paper_1607_03399_b200.distributed import DistributedLSERK
+
+    t_setup = time.perf_counter()
+    part = P.layered_slab(args.surface_n, [-1.0, -0.4, 0.2, 1.0], args.sublayers,
+                          [(1.0, 1.0), (1.0, 4.0), (1.0, 2.25)], ws, rank)
+    solver = DistributedLSERK(part, degree, device=local, threads=os.cpu_count() or 1)
+    d = solver.disc
+    s = pdg.make_initial_state(d, "gaussian", [0.25, 0.0, 0.0, 0.0])
+    dt = pdg.estimate_dt(d, 0.5)
+    t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    dt = float(t.item())
+    solver.set_state(s.u)
+    setup_s = time.perf_counter() - t_setup
+    solver.step(dt, args.warmup)
+    solver.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record(solver.stream)
+        solver.step(dt, args.steps)
+        stop.record(solver.stream)
+        stop.synchronize()
+    ms = start.elapsed_time(stop)
+    tt = torch.tensor([ms], device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = float(tt.item())
+    owned_dofs = 4 * d.info.np_wedge * part.n_owned
+    tot = torch.tensor([owned_dofs], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tot)
+    value = float(tot.item()) * args.steps / (ms / 1e3)
+    solver.close()
+    return {"degree": degree, "value": value, "ms_per_step": ms / args.steps, "total_dofs": owned_dofs,
+            "wedges": part.n_owned, "setup_s": round(setup_s, 1), "clocks": clk.summary(),
+            # per stage: one wedge stage kernel + one pack and one unpack per peer
+            "gpu_launches": args.steps * 5 * (1 + 2 * len(solver.peers)),
+            "exchange_bytes_per_stage": solver.exchange_bytes}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -270,6 +319,25 @@ def main():
     if ws > 1:
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks = load_peaks()
+    if ws > 1:
+        head = measure_degree_dist(args, args.degree, ws, rank, local, peaks)
+        if rank == 0:
+            line = {
+                "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (gaussian pulse on generated layered wedge mesh)",
+                "config": {"workload": "configs[4]: layered wedge slabs, 1e6 owned wedges per GPU stacked in z, "
+                                       "one ghost sublayer exchanged per LSERK stage (NCCL p2p)",
+                           "degree": args.degree, "wedges_per_gpu": head["wedges"],
+                           "parallelism": f"mesh partition x{ws}", "l2": "inputs larger than L2, no flush",
+                           "exchange_bytes_per_stage_per_rank": head["exchange_bytes_per_stage"]},
+                "roofline": None, "cpu_baseline": None, "e2e": None,
+                "gpu_launches": head["gpu_launches"], "clocks": head["clocks"], "setup_s": head["setup_s"],
+            }
+            print(json.dumps(line), flush=True)
+        torch.distributed.destroy_process_group()
+        return 0
     head = measure_degree(args, args.degree, ws, rank, local, peaks)
     sweep = []
     for deg in [int(x) for x in args.degrees.split(",") if x.strip()]:

@@ -67,6 +67,10 @@ int pdg_mesh_perturb_vertically(const pdg_mesh* in, double amplitude, uint64_t s
 int pdg_mesh_family(int family, double h, uint64_t seed, double xy_jitter, double z_amplitude,
                     double arnold_delta, pdg_mesh** out);                 /* analysis.cpp:110-124 */
 int pdg_mesh_spectra(uint64_t seed, double amplitude, pdg_mesh** out);   /* analysis.cpp:237-239 */
+/* a mesh from raw arrays (0-based ids, media[e] = {rho, kappa}); validated like
+ * load_mesh (mesh.cpp:487-516).  Used to build a rank's local mesh. */
+int pdg_mesh_from_arrays(int64_t nv, const double* vertices, int64_t nw, const int* wedges, int64_t nt,
+                         const int* tets, const double* media, pdg_mesh** out);
 int pdg_mesh_load(const char* path, pdg_mesh** out);                     /* mesh.hpp:117 */
 int pdg_mesh_save(const pdg_mesh* mesh, const char* path);               /* mesh.hpp:118 */
 /* counts[0..2] = vertices, wedges, tets */
@@ -157,6 +161,25 @@ int pdg_kernel_times(pdg_ctx* ctx, double* wedge_ms, int64_t* wedge_launches, do
 int pdg_stage_bytes(pdg_ctx* ctx, double* wedge_bytes, double* tet_bytes);
 /* number of device elements and the device element -> reference element map */
 int pdg_device_order(pdg_ctx* ctx, int64_t* dev_to_ref);
+
+/* ---------------------------------------------------------------- partitions
+ * Multi-GPU domain decomposition (no reference counterpart: SPEC.md:218 lists
+ * distributed runs as a non-goal; this is the north star's sharding).  A rank
+ * builds the discretization of its owned elements plus one ghost layer and
+ * passes owned[e] (one byte per element of that discretization).  Only owned
+ * elements are computed; before every LSERK stage the caller refreshes the
+ * ghosts' states from their owners (pack on the owner, transfer, unpack). */
+int pdg_create_partitioned(const pdg_disc* d, int device, int flags, const unsigned char* owned,
+                           pdg_ctx** out);
+/* counts[0..3] = owned wedges, owned tets, all wedges, all tets (device order:
+ * owned wedges, ghost wedges, owned tets, ghost tets) */
+int pdg_active_counts(pdg_ctx* ctx, int64_t counts[4]);
+/* one LSERK45 stage (0..4) of the resident state (TimeStepper::step, solver.cpp:543-550) */
+int pdg_step_stage(pdg_ctx* ctx, double dt, int stage);
+/* whole element states of the current state, device element ids and device
+ * buffers: buf[k * 4 * max(Np_wedge, Np_tet) + ...] = state of dev_elems[k] */
+int pdg_pack_states(pdg_ctx* ctx, const int64_t* dev_elems, int64_t n, double* buf);
+int pdg_unpack_states(pdg_ctx* ctx, const int64_t* dev_elems, int64_t n, const double* buf);
 
 /* ---------------------------------------------------------------- run driver */
 typedef struct {

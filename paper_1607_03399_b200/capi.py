@@ -99,6 +99,7 @@ SIGNATURES = {
     "pdg_mesh_perturb_vertically": (C.c_int, [P, C.c_double, C.c_uint64, PP]),
     "pdg_mesh_family": (C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_double, C.c_double, C.c_double, PP]),
     "pdg_mesh_spectra": (C.c_int, [C.c_uint64, C.c_double, PP]),
+    "pdg_mesh_from_arrays": (C.c_int, [C.c_int64, DP, C.c_int64, IP, C.c_int64, IP, DP, PP]),
     "pdg_mesh_load": (C.c_int, [C.c_char_p, PP]),
     "pdg_mesh_save": (C.c_int, [P, C.c_char_p]),
     "pdg_mesh_counts": (C.c_int, [P, I64P]),
@@ -137,6 +138,11 @@ SIGNATURES = {
     "pdg_stage_bytes": (C.c_int, [P, DP, DP]),
     "pdg_device_order": (C.c_int, [P, I64P]),
     "pdg_run_simulation": (C.c_int, [P, DP, DP, C.POINTER(RunOptions), C.POINTER(RunResult), DP, C.c_int]),
+    "pdg_create_partitioned": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(C.c_ubyte), PP]),
+    "pdg_active_counts": (C.c_int, [P, I64P]),
+    "pdg_step_stage": (C.c_int, [P, C.c_double, C.c_int]),
+    "pdg_pack_states": (C.c_int, [P, P, C.c_int64, P]),
+    "pdg_unpack_states": (C.c_int, [P, P, C.c_int64, P]),
 }
 
 

@@ -126,6 +126,25 @@ int pdg_mesh_spectra(uint64_t seed, double amplitude, pdg_mesh** out) {
   return guarded([&] { *out = wrap(spectra_mesh(seed, amplitude)); });
 }
 
+int pdg_mesh_from_arrays(int64_t nv, const double* vertices, int64_t nw, const int* wedges, int64_t nt,
+                         const int* tets, const double* media, pdg_mesh** out) {
+  return guarded([&] {
+    HybridMesh m;
+    m.vertices.resize(nv);
+    for (int64_t v = 0; v < nv; ++v) m.vertices[v] = {vertices[3 * v], vertices[3 * v + 1], vertices[3 * v + 2]};
+    m.wedges.resize(nw);
+    for (int64_t w = 0; w < nw; ++w)
+      for (int q = 0; q < 6; ++q) m.wedges[w][q] = wedges[6 * w + q];
+    m.tets.resize(nt);
+    for (int64_t t = 0; t < nt; ++t)
+      for (int q = 0; q < 4; ++q) m.tets[t][q] = tets[4 * t + q];
+    m.media.resize(nw + nt);
+    for (int64_t e = 0; e < nw + nt; ++e) m.media[e] = media_of(media ? media + 2 * e : nullptr);
+    validate_mesh(m);
+    *out = wrap(std::move(m));
+  });
+}
+
 int pdg_mesh_load(const char* path, pdg_mesh** out) {
   return guarded([&] { *out = wrap(load_mesh(path)); });
 }
@@ -352,6 +371,45 @@ int pdg_create(const pdg_disc* dh, int device, int flags, pdg_ctx** out) {
 }
 
 void pdg_destroy(pdg_ctx* ctx) { pdg::destroy_context(ctx); }
+
+int pdg_create_partitioned(const pdg_disc* dh, int device, int flags, const unsigned char* owned, pdg_ctx** out) {
+  return guarded([&] {
+    need(dh, "discretization");
+    need(owned, "owned mask");
+    *out = pdg::create_context(*D(dh), device, flags, owned);
+  });
+}
+
+int pdg_active_counts(pdg_ctx* ctx, int64_t counts[4]) {
+  return guarded([&] {
+    need(ctx, "context");
+    counts[0] = ctx->Kw_act;
+    counts[1] = ctx->Kt_act;
+    counts[2] = ctx->Kw;
+    counts[3] = ctx->Kt;
+  });
+}
+
+int pdg_step_stage(pdg_ctx* ctx, double dt, int stage) {
+  return guarded([&] {
+    need(ctx, "context");
+    pdg::stage_lserk(ctx, dt, stage);
+  });
+}
+
+int pdg_pack_states(pdg_ctx* ctx, const int64_t* dev_elems, int64_t n, double* buf) {
+  return guarded([&] {
+    need(ctx, "context");
+    pdg::pack_states(ctx, reinterpret_cast<const long long*>(dev_elems), n, buf);
+  });
+}
+
+int pdg_unpack_states(pdg_ctx* ctx, const int64_t* dev_elems, int64_t n, const double* buf) {
+  return guarded([&] {
+    need(ctx, "context");
+    pdg::unpack_states(ctx, reinterpret_cast<const long long*>(dev_elems), n, buf);
+  });
+}
 
 int pdg_set_state(pdg_ctx* ctx, const double* u, int on_device) {
   return guarded([&] {

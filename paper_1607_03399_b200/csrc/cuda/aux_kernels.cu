@@ -156,6 +156,26 @@ __global__ void check_finite_kernel(long long Kw, long long Kt, const double* __
   }
 }
 
+template <int N, bool PACK>
+__global__ void pack_kernel(long long Kw, const long long* __restrict__ elems, long long n,
+                            const double* __restrict__ src, double* __restrict__ dst) {
+  // one CTA per listed element; wedge and tet blocks have different sizes
+  constexpr int NPW = npw_of(N), NPT = npt_of(N);
+  for (long long q = blockIdx.x; q < n; q += gridDim.x) {
+    const long long d = elems[q];
+    const bool wedge = d < Kw;
+    const int len = 4 * (wedge ? NPW : NPT);
+    const long long off = wedge ? d * 4 * NPW : Kw * 4 * NPW + (d - Kw) * 4 * NPT;
+    const long long boff = q * 4 * (NPW > NPT ? NPW : NPT);
+    for (int k = threadIdx.x; k < len; k += blockDim.x) {
+      if (PACK)
+        dst[boff + k] = src[off + k];
+      else
+        dst[off + k] = src[boff + k];
+    }
+  }
+}
+
 int grid_for(long long total, int threads) {
   long long b = (total + threads - 1) / threads;
   if (b > 148 * 32) b = 148 * 32;
@@ -218,6 +238,22 @@ cudaError_t launch_energy(int N, const EnergyParams& p, int* nblocks_out, cudaSt
 
 cudaError_t launch_reduce_sum(const double* in, int n, double* out, cudaStream_t s) {
   reduce_sum_kernel<<<1, 1024, 0, s>>>(in, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_states(int N, long long Kw, const long long* dev_elems, long long n, const double* u,
+                               double* buf, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int grid = (int)(n < 148 * 16 ? n : 148 * 16);
+  PDG_DISPATCH(N, (pack_kernel<NN, true><<<grid, 128, 0, s>>>(Kw, dev_elems, n, u, buf)));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_states(int N, long long Kw, const long long* dev_elems, long long n, const double* buf,
+                                 double* u, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int grid = (int)(n < 148 * 16 ? n : 148 * 16);
+  PDG_DISPATCH(N, (pack_kernel<NN, false><<<grid, 128, 0, s>>>(Kw, dev_elems, n, buf, u)));
   return cudaGetLastError();
 }
 

@@ -150,6 +150,8 @@ StageParams base_params(pdg_ctx* c) {
   StageParams p{};
   p.Kw = c->Kw;
   p.Kt = c->Kt;
+  p.Kw_active = c->Kw_act;
+  p.Kt_active = c->Kt_act;
   p.tet_base = c->tet_base;
   p.wgeo = c->wgeo;
   p.wconn = c->wconn;
@@ -226,7 +228,7 @@ void upload_wedge_fragments(pdg_ctx* c, const prismdg::Discretization& d, const 
 
 } // namespace
 
-pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags) {
+pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags, const unsigned char* owned) {
   check_device(device);
   PDG_CK(cudaSetDevice(device));
   if (d.degree < 1 || d.degree > kMaxN) throw prismdg::ConfigError("degree out of range for device path");
@@ -251,8 +253,18 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags)
     const bool native = flags & 1;
 
     // ---- element order ------------------------------------------------------
-    const auto word = locality_order(d.mesh, true, native);
-    const auto tord = locality_order(d.mesh, false, native);
+    auto word = locality_order(d.mesh, true, native);
+    auto tord = locality_order(d.mesh, false, native);
+    c->Kw_act = c->Kw;
+    c->Kt_act = c->Kt;
+    if (owned) { // owned elements first, ghosts after (stable: keeps the locality order)
+      auto split = [&](std::vector<long long>& ord) {
+        std::stable_partition(ord.begin(), ord.end(), [&](long long r) { return owned[r] != 0; });
+        return (long long)std::count_if(ord.begin(), ord.end(), [&](long long r) { return owned[r] != 0; });
+      };
+      c->Kw_act = split(word);
+      c->Kt_act = split(tord);
+    }
     c->dev_to_ref_host.resize(c->Kw + c->Kt);
     std::copy(word.begin(), word.end(), c->dev_to_ref_host.begin());
     std::copy(tord.begin(), tord.end(), c->dev_to_ref_host.begin() + c->Kw);
@@ -450,11 +462,11 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags)
     const double wb_state_first = w8 * 3 * 4 * npw;  // u_in, res write, u_out
     const double wb_state_later = w8 * 4 * 4 * npw;  // + res read
     const double wb_ops = w8 * ((double)nt * nt + 3.0 * nt * nq + (34 + 2 * nq)) + 4.0 * kWC;
-    c->wedge_bytes_first = (double)c->Kw * (wb_state_first + wb_ops);
-    c->wedge_bytes_later = (double)c->Kw * (wb_state_later + wb_ops);
+    c->wedge_bytes_first = (double)c->Kw_act * (wb_state_first + wb_ops);
+    c->wedge_bytes_later = (double)c->Kw_act * (wb_state_later + wb_ops);
     const double tb_ops = w8 * 35 + 32.0;
-    c->tet_bytes_first = (double)c->Kt * (w8 * 3 * 4 * npt + tb_ops);
-    c->tet_bytes_later = (double)c->Kt * (w8 * 4 * 4 * npt + tb_ops);
+    c->tet_bytes_first = (double)c->Kt_act * (w8 * 3 * 4 * npt + tb_ops);
+    c->tet_bytes_later = (double)c->Kt_act * (w8 * 4 * 4 * npt + tb_ops);
     PDG_CK(cudaStreamSynchronize(c->stream));
   } catch (...) {
     destroy_context(c);
@@ -568,19 +580,46 @@ void step_lserk(pdg_ctx* c, double dt, int nsteps) {
     }
 }
 
+void stage_lserk(pdg_ctx* c, double dt, int s) {
+  PDG_CK(cudaSetDevice(c->device));
+  if (s < 0 || s > 4) throw prismdg::ConfigError("LSERK stage index must be in [0,5)");
+  StageParams p = base_params(c);
+  p.res = c->res;
+  p.dt = dt;
+  p.u_in = c->u[c->cur];
+  p.u_out = c->u[1 - c->cur];
+  p.a = kRK4A[s];
+  p.b = kRK4B[s];
+  p.mode = M_VOLUME | M_SURFACE | M_MEDIA | M_LSERK | (s == 0 ? M_FIRST : 0);
+  launch_checked(c, p, true);
+  launch_checked(c, p, false);
+  if (s == 0) ++c->stage_launches_first; else ++c->stage_launches_later;
+  c->cur = 1 - c->cur;
+}
+
+void pack_states(pdg_ctx* c, const long long* dev_elems, long long n, double* buf) {
+  PDG_CK(cudaSetDevice(c->device));
+  PDG_CK(launch_pack_states(c->N, c->Kw, dev_elems, n, c->u[c->cur], buf, c->stream));
+}
+
+void unpack_states(pdg_ctx* c, const long long* dev_elems, long long n, const double* buf) {
+  PDG_CK(cudaSetDevice(c->device));
+  PDG_CK(launch_unpack_states(c->N, c->Kw, dev_elems, n, buf, c->u[c->cur], c->stream));
+}
+
 double energy(pdg_ctx* c) {
   PDG_CK(cudaSetDevice(c->device));
   const int NT = c->nt;
   const int E = (256 / NT) > 0 ? 256 / NT : 1;
-  const int need = (int)((c->Kw + E - 1) / E + c->Kt) + 1;
+  const int need = (int)((c->Kw_act + E - 1) / E + c->Kt_act) + 1;
   if (need > c->partials_cap) {
     if (c->partials) cudaFree(c->partials);
     c->partials = dalloc<double>(need);
     c->partials_cap = need;
   }
   EnergyParams p{};
-  p.Kw = c->Kw;
-  p.Kt = c->Kt;
+  p.Kw = c->Kw_act; // owned elements only (ghosts belong to another rank)
+  p.Kt = c->Kt_act;
   p.tet_base = c->tet_base;
   p.u = c->u[c->cur];
   p.wgeo = c->wgeo;

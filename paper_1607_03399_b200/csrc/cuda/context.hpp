@@ -16,6 +16,7 @@ struct pdg_ctx {
   int flags = 0;
   int N = 0, nq = 0, nt = 0, npw = 0, npt = 0, fw = 0;
   long long Kw = 0, Kt = 0, total_dofs = 0, tet_base = 0;
+  long long Kw_act = 0, Kt_act = 0; // owned (computed) elements; ghosts follow them
   prismdg::MassMode mass_mode = prismdg::MassMode::exact;
 
   double* u[2] = {nullptr, nullptr};
@@ -67,8 +68,14 @@ struct pdg_ctx {
 
 namespace pdg {
 
-/// builds device buffers; throws prismdg::DeviceError on CUDA failures
-pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags);
+/// builds device buffers; throws prismdg::DeviceError on CUDA failures.  With
+/// `owned` (one flag per reference element) only owned elements are computed;
+/// ghosts are ordered after the owned elements of their kind.
+pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags,
+                        const unsigned char* owned = nullptr);
+void stage_lserk(pdg_ctx* c, double dt, int stage);
+void pack_states(pdg_ctx* c, const long long* dev_elems, long long n, double* buf);
+void unpack_states(pdg_ctx* c, const long long* dev_elems, long long n, const double* buf);
 void destroy_context(pdg_ctx* c);
 void set_state(pdg_ctx* c, const double* u, bool on_device);
 void get_state(pdg_ctx* c, double* u, bool on_device);

@@ -66,7 +66,8 @@ enum : int {
 };
 
 struct StageParams {
-  long long Kw, Kt;
+  long long Kw, Kt;               // all device elements (addressing)
+  long long Kw_active, Kt_active; // elements computed: owned ones come first, ghosts after
   long long tet_base; // dof offset of the first tet block
   const double* __restrict__ u_in;
   double* __restrict__ u_out;
@@ -130,6 +131,11 @@ cudaError_t launch_to_device_layout(int N, long long Kw, long long Kt, const int
 cudaError_t launch_to_reference_layout(int N, long long Kw, long long Kt, const int* dev_to_ref,
                                        const long long* ref_offset, const double* src_dev,
                                        double* dst_ref, cudaStream_t s);
+/// gather / scatter whole element states (halo exchange): buf[k] = state of dev_elems[k]
+cudaError_t launch_pack_states(int N, long long Kw, const long long* dev_elems, long long n, const double* u,
+                               double* buf, cudaStream_t s);
+cudaError_t launch_unpack_states(int N, long long Kw, const long long* dev_elems, long long n, const double* buf,
+                                 double* u, cudaStream_t s);
 cudaError_t launch_check_finite(int N, long long Kw, long long Kt, const double* u,
                                 const int* dev_to_ref, unsigned long long* first_bad,
                                 cudaStream_t s);

@@ -212,12 +212,12 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
   if (tt == 0) {
     const long long e0 = grab();
     slot[0] = e0;
-    if (e0 < p.Kw) load_element<N, NST>(p, stg0, e0, res_src, bar);
+    if (e0 < p.Kw_active) load_element<N, NST>(p, stg0, e0, res_src, bar);
   }
   team_sync(bar_id, 32 * T);
   long long e = slot[0];
 
-  for (int n = 0; e < p.Kw; ++n) {
+  for (int n = 0; e < p.Kw_active; ++n) {
     const int s = NST == 2 ? (n & 1) : 0;
     long long en = 0;
     if (tt == 0) {
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
     const double* Qf = Lf + C::LF;
     const double* G = Qf + C::QF;
     const int* Cn = reinterpret_cast<const int*>(G + WG);
-    if (NST == 2 && tt == 0 && en < p.Kw) {
+    if (NST == 2 && tt == 0 && en < p.Kw_active) {
       fence_proxy_async_smem();
       load_element<N, NST>(p, stg0 + (s ^ 1) * C::STAGE, en, res_src, bar + (s ^ 1));
     }
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
         }
     }
     team_sync(bar_id, 32 * T); // stage s and the work buffers are free again
-    if (NST == 1 && tt == 0 && en < p.Kw) load_element<N, NST>(p, stg0, en, res_src, bar);
+    if (NST == 1 && tt == 0 && en < p.Kw_active) load_element<N, NST>(p, stg0, en, res_src, bar);
     e = slot[1];
     team_sync(bar_id, 32 * T); // slot[1] is read by every thread before it is rewritten
   }
@@ -492,12 +492,12 @@ cudaError_t launch_dmma_NC(const StageParams& p, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM_BYTES);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
-  if (p.Kw == 0) return cudaSuccess;
-  const long long need = (p.Kw + C::TPB - 1) / C::TPB;
+  if (p.Kw_active == 0) return cudaSuccess;
+  const long long need = (p.Kw_active + C::TPB - 1) / C::TPB;
   const int grid = (int)(need < grid_cap ? need : grid_cap);
   StageParams q = p;
   q.ticket_base = *p.ticket_host_next;
-  *p.ticket_host_next += (unsigned long long)p.Kw + (unsigned long long)grid * C::TPB;
+  *p.ticket_host_next += (unsigned long long)p.Kw_active + (unsigned long long)grid * C::TPB;
   kern<<<grid, C::THREADS, C::SMEM_BYTES, s>>>(q);
   return cudaGetLastError();
 }

@@ -114,6 +114,14 @@ def spectra_mesh(seed=42, amplitude=0.3):
     return _mesh_from(lib().pdg_mesh_spectra, seed, amplitude)
 
 
+def mesh_from_arrays(vertices, wedges, tets, media):
+    v = np.ascontiguousarray(vertices, dtype=np.float64).reshape(-1, 3)
+    w = np.ascontiguousarray(wedges, dtype=np.int32).reshape(-1, 6)
+    t = np.ascontiguousarray(tets, dtype=np.int32).reshape(-1, 4)
+    m = np.ascontiguousarray(media, dtype=np.float64).reshape(-1, 2)
+    return _mesh_from(lib().pdg_mesh_from_arrays, v.shape[0], _dp(v), w.shape[0], _ip(w), t.shape[0], _ip(t), _dp(m))
+
+
 def load_mesh(path: str):
     return _mesh_from(lib().pdg_mesh_load, path.encode())
 
