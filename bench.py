@@ -172,8 +172,15 @@ def measure_degree(args, degree, ws, rank, local, peaks, with_e2e=True):
     import paper_1607_03399_b200 as pdg
 
     t_setup = time.perf_counter()
-    mesh = layered_workload(args.surface_n, args.sublayers)
-    d = pdg.build_discretization(mesh, degree, threads=os.cpu_count() or 1)
+    if getattr(args, "workload", "layered") == "hybrid":
+        # configs[2]: structured_hybrid_box(64,64,32,32) = 262,144 wedges + 786,432 tets
+        mesh = pdg.structured_hybrid_box(args.hybrid_n, args.hybrid_n, args.hybrid_n // 2, args.hybrid_n // 2,
+                                         (1.0, 1.0), (1.0, 4.0))
+    else:
+        mesh = layered_workload(args.surface_n, args.sublayers)
+    mass = getattr(args, "mass", "exact")
+    d = pdg.build_discretization(mesh, degree, threads=os.cpu_count() or 1, mass=mass,
+                                 host_lifts=(mass != "wadg"))
     s = pdg.make_initial_state(d, "gaussian", [0.25, 0.0, 0.0, 0.0])
     dt = pdg.estimate_dt(d, 0.5)
     ctx = pdg.DeviceContext(d, device=local, flags=pdg.capi.CTX_TIMING)
@@ -206,7 +213,8 @@ def measure_degree(args, degree, ws, rank, local, peaks, with_e2e=True):
     dofs = d.total_dofs
     value = dofs * args.steps * ws / (ms / 1e3)
     wedge_avg_ms = kt["wedge_ms"] / max(1, kt["wedge_launches"])
-    achieved = wbytes / (wedge_avg_ms / 1e3) / 1e9
+    achieved = wbytes / (wedge_avg_ms / 1e3) / 1e9 if wedge_avg_ms > 0 else 0.0
+    tet_avg_ms = kt["tet_ms"] / max(1, kt["tet_launches"])
     res = {
         "degree": degree, "value": value, "ms_per_step": ms / args.steps, "total_dofs": dofs,
         "wedges": mesh.num_wedges(), "setup_s": round(setup_s, 1),
@@ -215,8 +223,15 @@ def measure_degree(args, degree, ws, rank, local, peaks, with_e2e=True):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks[0], "unit": "GB/s",
                      "frac": achieved / peaks[0], "traffic": None, "peak_source": peaks[1]},
         "gpu_launches": int(kt["wedge_launches"] + kt["tet_launches"]),
+        "tets": mesh.num_tets(),
         "clocks": clk.summary(),
     }
+    if mesh.num_tets() > 0:
+        t_ach = tbytes / (tet_avg_ms / 1e3) / 1e9
+        res["tet_kernel_avg_ms"] = tet_avg_ms
+        res["tet_kernel_share"] = kt["tet_ms"] / ms if ms > 0 else None
+        res["tet_roofline"] = {"bound": "hbm", "achieved": t_ach, "peak": peaks[0], "unit": "GB/s",
+                               "frac": t_ach / peaks[0], "traffic": None, "peak_source": peaks[1]}
     if with_e2e:
         # e2e through the C ABI: pinned host state in, one step, state out, every step
         host = torch.empty(dofs, dtype=torch.float64, pin_memory=True)
@@ -306,6 +321,11 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="layered", choices=["layered", "hybrid"],
+                    help="layered = configs[1] (1e6 wedges); hybrid = configs[2] (wedge layers over a tet cap)")
+    ap.add_argument("--hybrid-n", type=int, default=64)
+    ap.add_argument("--mass", default="exact", choices=["exact", "wadg"],
+                    help="exact stored-lift mass (reference parity mode) or weight-adjusted (north-star WADG)")
     args = ap.parse_args()
     args.sublayers = [int(x) for x in args.sublayers.split(",")]
     args.warmup = max(3, args.warmup)
@@ -345,7 +365,7 @@ def main():
             continue
         r = measure_degree(args, deg, ws, rank, local, peaks, with_e2e=False)
         sweep.append({k: r[k] for k in ("degree", "value", "ms_per_step", "wedge_kernel_avg_ms", "roofline",
-                                        "total_dofs", "setup_s")})
+                                        "total_dofs", "setup_s", "gpu_launches")})
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -357,14 +377,20 @@ def main():
             "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (gaussian pulse on generated layered wedge mesh, random-free)",
-            "config": {"workload": "configs[1]: layered wedge mesh, stack_layers n=100 surface x 50 sublayers "
-                                   "(1e6 wedges/GPU), exact stored-lift mass, upwind",
+            "config": {"workload": (f"configs[2]: structured_hybrid_box({args.hybrid_n},{args.hybrid_n},"
+                                    f"{args.hybrid_n // 2},{args.hybrid_n // 2}), {head['wedges']} wedges + "
+                                    f"{head['tets']} tets, " if args.workload == "hybrid" else
+                                    "configs[1]: layered wedge mesh, stack_layers n=100 surface x 50 sublayers "
+                                   "(1e6 wedges/GPU), ") + ("exact stored-lift mass" if args.mass == "exact" else
+                                   "weight-adjusted (WADG) mass, no per-wedge operator storage") + ", upwind",
+                       "mass": args.mass,
                        "degree": args.degree, "wedges_per_gpu": head["wedges"], "total_dofs_per_gpu": head["total_dofs"],
                        "parallelism": f"mesh partition x{ws}" if ws > 1 else "single GPU",
                        "l2": "inputs larger than L2 (state >> 126 MB), no flush"},
             "roofline": head["roofline"], "cpu_baseline": cpu, "e2e": head.get("e2e"),
             "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
             "wedge_kernel_avg_ms": head["wedge_kernel_avg_ms"], "wedge_kernel_share": head["wedge_kernel_share"],
+            **({k: head[k] for k in ("tet_kernel_avg_ms", "tet_kernel_share", "tet_roofline") if k in head}),
             "setup_s": head["setup_s"],
         }
         if sweep:

@@ -37,7 +37,8 @@ extern "C" {
 
 #define PDG_MASS_EXACT 0  /* QuadratureMode::exact  (operators.hpp:17) */
 #define PDG_MASS_LUMPED 1 /* QuadratureMode::lumped                      */
-#define PDG_MASS_WADG 2   /* weight-adjusted inverse (north-star extension) */
+#define PDG_MASS_WADG 2   /* weight-adjusted inverse Mhat^-1 M_{1/J} Mhat^-1 (north-star
+                             extension; tets stay exact) */
 
 typedef struct pdg_mesh pdg_mesh; /* prismdg::HybridMesh      (mesh.hpp:22-41)   */
 typedef struct pdg_disc pdg_disc; /* prismdg::Discretization  (solver.hpp:29-59) */
@@ -92,6 +93,13 @@ typedef struct {
 /* build_discretization (solver.hpp:61-63). threads = OpenMP threads for setup. */
 int pdg_disc_build(const pdg_mesh* mesh, int degree, int flux_mode, double tau_p, double tau_u,
                    int mass_mode, int threads, pdg_disc** out);
+/* build_discretization with flags.  PDG_DISC_NO_HOST_LIFTS (WADG only): do
+ * not build the per-wedge exact lifts on the host either -- the reduced
+ * storage of the weight-adjusted mode end to end (the CPU oracle cannot run
+ * on such a discretization). */
+#define PDG_DISC_NO_HOST_LIFTS 1
+int pdg_disc_build_ex(const pdg_mesh* mesh, int degree, int flux_mode, double tau_p, double tau_u,
+                      int mass_mode, int threads, int flags, pdg_disc** out);
 int pdg_disc_get_info(const pdg_disc* d, pdg_disc_info* info);
 /* Discretization::elem_offset (solver.hpp:44), num_elements+1 entries */
 int pdg_disc_elem_offset(const pdg_disc* d, int64_t* out);

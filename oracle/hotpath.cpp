@@ -266,6 +266,53 @@ void surface_elem(const Discretization& d, int e, const double* u, double* rhs, 
   }
 }
 
+// ---- weight-adjusted (WADG) mode: an extension of the reference (SURVEY.md
+// A.4).  Restated independently of the device factorisation: the exact system
+// is M_k du/dt = S u + B with M_k = M^{tri,k} (x) M1D, so the WADG rhs is
+//   Mtilde^{-1} M_k rhs_exact = (Mhat^{-1} M_{1/J} Mhat^{-1} M^{tri,k}) (x) I
+// applied to the exact rhs, slice by slice, with M_{1/J} assembled here on the
+// reference triangle cubature.  Tets are affine: WADG == exact there.
+Mat inv_j_mass(const Discretization& d, int w) {
+  const auto& tri = d.refs.tri;
+  const WedgeGeo& g = d.wgeo[w];
+  const int nt = d.nt, nc = (int)tri.cubature.weights.size();
+  Mat m(nt, nt);
+  for (int q = 0; q < nc; ++q) {
+    const double J = g.j0 + g.jr * tri.cubature.points(q, 0) + g.js * tri.cubature.points(q, 1);
+    for (int a = 0; a < nt; ++a)
+      for (int b = 0; b < nt; ++b) m(a, b) += tri.cubature.weights[q] * tri.interp_cub(q, a) * tri.interp_cub(q, b) / J;
+  }
+  return m;
+}
+
+Mat wadg_transform_matrix(const Discretization& d, int w) {
+  const Mat minv = inverse(d.refs.tri.mass);
+  const WedgeGeo& g = d.wgeo[w];
+  const Mat mk = wedge_tri_mass(g.j0, g.jr, g.js, d.refs);
+  return matmul(matmul(minv, inv_j_mass(d, w)), matmul(minv, mk));
+}
+
+// block of one wedge (4 fields, node i*nq + j): x_j <- T x_j for every slice j
+void wadg_apply(const Discretization& d, int w, double* block) {
+  const int nq = d.nq, nt = d.nt, np = d.np_wedge;
+  const Mat T = wadg_transform_matrix(d, w);
+  std::vector<double> tmp(nt);
+  for (int f = 0; f < 4; ++f)
+    for (int j = 0; j < nq; ++j) {
+      double* x = block + (std::size_t)f * np;
+      for (int i = 0; i < nt; ++i) {
+        double s = 0.0;
+        for (int k = 0; k < nt; ++k) s += T(i, k) * x[k * nq + j];
+        tmp[i] = s;
+      }
+      for (int i = 0; i < nt; ++i) x[i * nq + j] = tmp[i];
+    }
+}
+
+inline bool is_wadg_wedge(const Discretization& d, int e) {
+  return d.mass_mode == MassMode::wadg && d.mesh.kind(e) == ElemKind::wedge;
+}
+
 void scale_media(const Discretization& d, int e, double* rhs) {
   const int np = d.np(e);
   const std::size_t base = d.elem_offset[e];
@@ -301,6 +348,7 @@ void compute_rhs(const Discretization& d, const double* u, double* rhs, int thre
       else
         tet_volume_elem(d, e, u, rhs, ws);
       surface_elem(d, e, u, rhs, ws);
+      if (is_wadg_wedge(d, e)) wadg_apply(d, e, rhs + d.elem_offset[e]);
       scale_media(d, e, rhs);
     }
   }
@@ -308,11 +356,26 @@ void compute_rhs(const Discretization& d, const double* u, double* rhs, int thre
 
 void wedge_volume_phase(const Discretization& d, const double* u, double* rhs) {
   Scratch ws = make_scratch(d);
-  for (int e = 0; e < d.mesh.num_wedges(); ++e) wedge_volume_elem(d, e, u, rhs, ws);
+  for (int e = 0; e < d.mesh.num_wedges(); ++e) {
+    wedge_volume_elem(d, e, u, rhs, ws);
+    if (is_wadg_wedge(d, e)) wadg_apply(d, e, rhs + d.elem_offset[e]);
+  }
 }
 void wedge_surface_phase(const Discretization& d, const double* u, double* rhs) {
   Scratch ws = make_scratch(d);
-  for (int e = 0; e < d.mesh.num_wedges(); ++e) surface_elem(d, e, u, rhs, ws);
+  for (int e = 0; e < d.mesh.num_wedges(); ++e) {
+    if (!is_wadg_wedge(d, e)) {
+      surface_elem(d, e, u, rhs, ws);
+      continue;
+    }
+    // WADG is linear: accumulate T * (surface part)
+    double* blk = rhs + d.elem_offset[e];
+    const std::vector<double> saved(blk, blk + 4 * d.np_wedge);
+    std::fill(blk, blk + 4 * d.np_wedge, 0.0);
+    surface_elem(d, e, u, rhs, ws);
+    wadg_apply(d, e, blk);
+    for (int n = 0; n < 4 * d.np_wedge; ++n) blk[n] += saved[n];
+  }
 }
 void tet_volume_phase(const Discretization& d, const double* u, double* rhs) {
   Scratch ws = make_scratch(d);
@@ -335,7 +398,19 @@ double compute_energy(const Discretization& d, const double* u, int threads) {
     double acc = 0.0;
     for (int field = 0; field < 4; ++field) {
       Vec v(u + base + field * np, u + base + (field + 1) * np), mu;
-      if (d.mesh.kind(e) == ElemKind::wedge) {
+      if (is_wadg_wedge(d, e)) {
+        // Mtilde = (Mhat M_{1/J}^{-1} Mhat) (x) M1D
+        const Mat mt = matmul(matmul(d.refs.tri.mass, inverse(inv_j_mass(d, e))), d.refs.tri.mass);
+        const int nq = d.nq, nt = d.nt;
+        mu.assign(np, 0.0);
+        for (int i = 0; i < nt; ++i)
+          for (int j = 0; j < nq; ++j) {
+            double s = 0.0;
+            for (int k = 0; k < nt; ++k)
+              for (int l = 0; l < nq; ++l) s += mt(i, k) * d.refs.line.mass(j, l) * v[k * nq + l];
+            mu[i * nq + j] = s;
+          }
+      } else if (d.mesh.kind(e) == ElemKind::wedge) {
         const ElementGeometry g = d.geometry(e);
         apply_wedge_mass(g, d.refs, d.qmode, v, mu);
       } else {

@@ -107,6 +107,8 @@ SIGNATURES = {
     "pdg_mesh_volume": (C.c_int, [P, DP]),
     "pdg_mesh_free": (None, [P]),
     "pdg_disc_build": (C.c_int, [P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, PP]),
+    "pdg_disc_build_ex": (C.c_int, [P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
+                                    PP]),
     "pdg_disc_get_info": (C.c_int, [P, C.POINTER(DiscInfo)]),
     "pdg_disc_elem_offset": (C.c_int, [P, I64P]),
     "pdg_disc_face_table": (C.c_int, [P, IP, IP, IP]),

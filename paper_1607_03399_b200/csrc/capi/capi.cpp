@@ -198,11 +198,17 @@ void pdg_mesh_free(pdg_mesh* mesh) { delete M(mesh); }
 // ------------------------------------------------------------------ discretization
 int pdg_disc_build(const pdg_mesh* mesh, int degree, int flux_mode, double tau_p, double tau_u,
                    int mass_mode, int threads, pdg_disc** out) {
+  return pdg_disc_build_ex(mesh, degree, flux_mode, tau_p, tau_u, mass_mode, threads, 0, out);
+}
+
+int pdg_disc_build_ex(const pdg_mesh* mesh, int degree, int flux_mode, double tau_p, double tau_u,
+                      int mass_mode, int threads, int flags, pdg_disc** out) {
   return guarded([&] {
     need(mesh, "mesh");
     if (flux_mode < 0 || flux_mode > 2) throw ConfigError("unknown flux mode");
     if (mass_mode < 0 || mass_mode > 2) throw ConfigError("unknown mass mode");
-    if (mass_mode == PDG_MASS_WADG) throw ConfigError("weight-adjusted mass is not available in this build");
+    if ((flags & PDG_DISC_NO_HOST_LIFTS) && mass_mode != PDG_MASS_WADG)
+      throw ConfigError("PDG_DISC_NO_HOST_LIFTS requires the weight-adjusted mass mode");
     FluxConfig flux;
     flux.mode = static_cast<FluxMode>(flux_mode);
     flux.tau_p = tau_p;
@@ -212,7 +218,8 @@ int pdg_disc_build(const pdg_mesh* mesh, int degree, int flux_mode, double tau_p
     if (threads > 0) omp_set_num_threads(threads);
 #endif
     auto* d = new Discretization(build_discretization(*M(mesh), degree, flux, qm, std::max(1, threads),
-                                                      static_cast<MassMode>(mass_mode), true));
+                                                      static_cast<MassMode>(mass_mode),
+                                                      !(flags & PDG_DISC_NO_HOST_LIFTS)));
     *out = reinterpret_cast<pdg_disc*>(d);
   });
 }
@@ -347,6 +354,7 @@ int pdg_disc_wedge_ops(const pdg_disc* dh, int64_t w, double* tri_lift, double* 
     const Discretization& d = *D(dh);
     if (w < 0 || w >= d.mesh.num_wedges()) throw ConfigError("wedge index out of range");
     const std::size_t nt2 = (std::size_t)d.nt * d.nt, nql = (std::size_t)3 * d.nq * d.nt;
+    if (tri_lift && d.tri_lift.empty()) throw ConfigError("discretization was built without host lifts");
     if (tri_lift) std::copy(d.tri_lift.begin() + w * nt2, d.tri_lift.begin() + (w + 1) * nt2, tri_lift);
     if (quad_lift && !d.quad_lift.empty())
       std::copy(d.quad_lift.begin() + w * nql, d.quad_lift.begin() + (w + 1) * nql, quad_lift);

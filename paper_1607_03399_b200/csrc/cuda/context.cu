@@ -138,7 +138,8 @@ void launch_checked(pdg_ctx* c, const StageParams& p, bool wedge) {
     PDG_CK(cudaEventCreate(&b));
     PDG_CK(cudaEventRecord(a, c->stream));
   }
-  cudaError_t err = wedge ? launch_wedge_stage(c->N, p, c->stream) : launch_tet_stage(c->N, p, c->stream);
+  cudaError_t err = !wedge ? launch_tet_stage(c->N, p, c->stream)
+                    : (c->wadg ? launch_wedge_wadg_stage(c->N, p, c->stream) : launch_wedge_stage(c->N, p, c->stream));
   if (err != cudaSuccess) throw DeviceError(std::string("stage kernel launch failed: ") + cudaGetErrorString(err));
   if (c->flags & 2) {
     PDG_CK(cudaEventRecord(b, c->stream));
@@ -157,6 +158,7 @@ StageParams base_params(pdg_ctx* c) {
   p.wconn = c->wconn;
   p.Lt = c->Lt;
   p.QL = c->QL;
+  p.wadg = c->wadg;
   p.tgeo = c->tgeo;
   p.tconn = c->tconn;
   p.DrT = c->DrT;
@@ -224,6 +226,38 @@ void upload_wedge_fragments(pdg_ctx* c, const prismdg::Discretization& d, const 
     PDG_CK(cudaMemcpy(c->QL + c0 * QF, pq, cn * QF * 8, cudaMemcpyHostToDevice));
   }
   cudaFreeHost(pin);
+}
+
+// WADG shared tables in the flat layout of pdg_device.cuh (wadg_off_*)
+std::vector<double> flatten_wadg(const prismdg::Discretization& d) {
+  const int N = d.degree, nt = d.nt, nq = d.nq, nc = wadg_nc(N);
+  const prismdg::WadgTables w = prismdg::build_wadg_tables(d.refs);
+  if (w.nc != nc) throw prismdg::ConfigError("unexpected triangle cubature size for WADG");
+  std::vector<double> f((std::size_t)wadg_size(N), 0.0);
+  for (int m = 0; m < 6; ++m)
+    for (int i = 0; i < nt; ++i)
+      for (int k = 0; k < nt; ++k) f[((std::size_t)m * nt + i) * nt + k] = w.kd[m](i, k);
+  for (int i = 0; i < nt; ++i)
+    for (int q = 0; q < nc; ++q) {
+      f[wadg_off_pw(N) + (std::size_t)i * nc + q] = w.Pw(i, q);
+      f[wadg_off_vq(N) + (std::size_t)q * nt + i] = w.Vq(q, i);
+    }
+  for (int e = 0; e < 3; ++e)
+    for (int i = 0; i < nt; ++i)
+      for (int a = 0; a < nq; ++a) {
+        f[wadg_off_r(N) + ((std::size_t)(0 * 3 + e) * nt + i) * nq + a] = w.R0[e](i, a);
+        f[wadg_off_r(N) + ((std::size_t)(1 * 3 + e) * nt + i) * nq + a] = w.R1[e](i, a);
+      }
+  for (int q = 0; q < nc; ++q) {
+    f[wadg_off_q(N) + q] = w.qr[q];
+    f[wadg_off_q(N) + nc + q] = w.qs[q];
+    f[wadg_off_q(N) + 2 * nc + q] = d.refs.tri.cubature.weights[q];
+  }
+  for (int i = 0; i < nt; ++i)
+    for (int k = 0; k < nt; ++k) f[wadg_off_mhat(N) + (std::size_t)i * nt + k] = d.refs.tri.mass(i, k);
+  for (int j = 0; j < nq; ++j)
+    for (int l = 0; l < nq; ++l) f[wadg_off_m1d(N) + (std::size_t)j * nq + l] = d.refs.line.mass(j, l);
+  return f;
 }
 
 } // namespace
@@ -339,11 +373,17 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags,
       }
       c->wgeo = upload(geo);
       c->wconn = upload(conn);
-      std::vector<long long> word0(word);
-      if (c->Kw > 0 && d.quad_lift.empty()) throw prismdg::ConfigError("device path needs the quad lifts");
-      c->Lt = dalloc<double>((std::size_t)c->Kw * lfrag_of(N));
-      c->QL = dalloc<double>((std::size_t)c->Kw * qfrag_of(N));
-      upload_wedge_fragments(c, d, word0);
+      if (d.mass_mode == prismdg::MassMode::wadg) {
+        // reduced storage: shared tables only, nothing per wedge beyond the record
+        if (N > 7) throw prismdg::ConfigError("the WADG device path supports degrees 1..7");
+        c->wadg = upload(flatten_wadg(d));
+      } else {
+        std::vector<long long> word0(word);
+        if (c->Kw > 0 && d.quad_lift.empty()) throw prismdg::ConfigError("device path needs the quad lifts");
+        c->Lt = dalloc<double>((std::size_t)c->Kw * lfrag_of(N));
+        c->QL = dalloc<double>((std::size_t)c->Kw * qfrag_of(N));
+        upload_wedge_fragments(c, d, word0);
+      }
     }
 
     // ---- tet records ------------------------------------------------------------
@@ -461,7 +501,9 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags,
     const double w8 = 8.0;
     const double wb_state_first = w8 * 3 * 4 * npw;  // u_in, res write, u_out
     const double wb_state_later = w8 * 4 * 4 * npw;  // + res read
-    const double wb_ops = w8 * ((double)nt * nt + 3.0 * nt * nq + (34 + 2 * nq)) + 4.0 * kWC;
+    // exact: L^{tri,k} + quad lifts + record; WADG: the record only
+    const double wb_ops = c->wadg ? w8 * wg_of(N) + 4.0 * kWC
+                                  : w8 * ((double)nt * nt + 3.0 * nt * nq + (34 + 2 * nq)) + 4.0 * kWC;
     c->wedge_bytes_first = (double)c->Kw_act * (wb_state_first + wb_ops);
     c->wedge_bytes_later = (double)c->Kw_act * (wb_state_later + wb_ops);
     const double tb_ops = w8 * 35 + 32.0;
@@ -483,7 +525,7 @@ void destroy_context(pdg_ctx* c) {
     cudaEventDestroy(pe.a);
     cudaEventDestroy(pe.b);
   }
-  void* ptrs[] = {c->u[0], c->u[1], c->res, c->rhs, c->stage, c->wgeo, c->wconn, c->Lt, c->QL,
+  void* ptrs[] = {c->u[0], c->u[1], c->res, c->rhs, c->stage, c->wgeo, c->wconn, c->Lt, c->QL, c->wadg,
                   c->tgeo, c->tconn, c->DrT, c->DsT, c->Dt, c->prof, c->wface_dev, c->tDrT,
                   c->tDsT, c->tDtT, c->tLiftT, c->tface, c->nbr_nodes, c->Mtri, c->Xr, c->Xs,
                   c->M1D, c->w1d, c->Mtet, c->partials, c->scalar, c->badflag, c->ticket, c->dev_to_ref,
@@ -611,7 +653,7 @@ double energy(pdg_ctx* c) {
   PDG_CK(cudaSetDevice(c->device));
   const int NT = c->nt;
   const int E = (256 / NT) > 0 ? 256 / NT : 1;
-  const int need = (int)((c->Kw_act + E - 1) / E + c->Kt_act) + 1;
+  const int need = (int)((c->Kw_act + E - 1) / E + (c->Kw_act + 3) / 4 + c->Kt_act) + 1;
   if (need > c->partials_cap) {
     if (c->partials) cudaFree(c->partials);
     c->partials = dalloc<double>(need);
@@ -631,9 +673,21 @@ double energy(pdg_ctx* c) {
   p.w1d = c->w1d;
   p.Mtet = c->Mtet;
   p.lumped = c->mass_mode == prismdg::MassMode::lumped;
+  p.wadg = c->wadg;
   p.partials = c->partials;
   int nb = 0;
-  PDG_CK(launch_energy(c->N, p, &nb, c->stream));
+  if (c->wadg) {
+    // wedges in the Mtilde norm (one partial per 4 wedges), then the tets
+    int nbw = 0, nbt = 0;
+    PDG_CK(launch_wadg_energy(c->N, p, &nbw, c->stream));
+    EnergyParams pt = p;
+    pt.Kw = 0;
+    pt.partials = c->partials + nbw;
+    PDG_CK(launch_energy(c->N, pt, &nbt, c->stream));
+    nb = nbw + nbt;
+  } else {
+    PDG_CK(launch_energy(c->N, p, &nb, c->stream));
+  }
   if (nb == 0) return 0.0;
   PDG_CK(launch_reduce_sum(c->partials, nb, c->scalar, c->stream));
   double e = 0.0;

@@ -29,6 +29,7 @@ struct pdg_ctx {
   int* wconn = nullptr;
   double* Lt = nullptr;
   double* QL = nullptr;
+  double* wadg = nullptr; // WADG shared tables (mass_mode == wadg)
   double* tgeo = nullptr;
   int* tconn = nullptr;
 

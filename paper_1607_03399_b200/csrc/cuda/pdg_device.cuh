@@ -38,6 +38,23 @@ __host__ __device__ constexpr int lfrag_of(int N) { return it_of(N) * ks_of(N) *
 /// per-wedge quad lifts: [t][face][s][lane] = QL_face(8t+lane/4, 4s+lane%4)
 __host__ __device__ constexpr int qfrag_of(int N) { return it_of(N) * 3 * kt_of(N) * 32; }
 
+// Weight-adjusted (WADG) shared tables, one flat array (built by the context
+// from prismdg::WadgTables, operators.hpp): row-major
+//   kd[6][nt][nt]  Dr, Kr Dr, Ks Dr, Ds, Kr Ds, Ks Ds
+//   Pw[nt][nc]     Mhat^{-1} V_q^T diag(w_q)
+//   Vq[nc][nt]     triangle basis at the cubature points
+//   R[2][3][nt][nq] quad-face lifts before Ltilde: jf0 R[0][e] + jf1 R[1][e]
+//   qr[nc], qs[nc], wq[nc]  cubature points and weights
+//   Mhat[nt][nt], M1D[nq][nq]
+__host__ __device__ constexpr int wadg_nc(int N) { return (N + 2) * (N + 2); }
+__host__ __device__ constexpr int wadg_off_pw(int N) { return 6 * nt_of(N) * nt_of(N); }
+__host__ __device__ constexpr int wadg_off_vq(int N) { return wadg_off_pw(N) + nt_of(N) * wadg_nc(N); }
+__host__ __device__ constexpr int wadg_off_r(int N) { return wadg_off_vq(N) + nt_of(N) * wadg_nc(N); }
+__host__ __device__ constexpr int wadg_off_q(int N) { return wadg_off_r(N) + 6 * nt_of(N) * nq_of(N); }
+__host__ __device__ constexpr int wadg_off_mhat(int N) { return wadg_off_q(N) + 3 * wadg_nc(N); }
+__host__ __device__ constexpr int wadg_off_m1d(int N) { return wadg_off_mhat(N) + nt_of(N) * nt_of(N); }
+__host__ __device__ constexpr int wadg_size(int N) { return wadg_off_m1d(N) + nq_of(N) * nq_of(N); }
+
 // wedge record offsets
 enum WRec : int {
   W_RX = 0, W_RY, W_SX, W_SY, W_TZJ, W_JFB, W_JFT, W_KAPPA, W_IRHO,
@@ -80,6 +97,7 @@ struct StageParams {
   const int* __restrict__ wconn;
   const double* __restrict__ Lt;
   const double* __restrict__ QL;
+  const double* __restrict__ wadg; // WADG shared tables (null unless the mass mode is wadg)
   // tets
   const double* __restrict__ tgeo;
   const int* __restrict__ tconn;
@@ -115,12 +133,16 @@ struct EnergyParams {
   const double* __restrict__ w1d;   // GLL weights
   const double* __restrict__ Mtet;  // [npt][npt]
   int lumped;
+  const double* __restrict__ wadg; // non-null: wedges use the weight-adjusted mass
   double* __restrict__ partials;
 };
 
 // launchers (instantiated per degree in the .cu files)
 cudaError_t launch_wedge_stage(int N, const StageParams& p, cudaStream_t s); // FP64 tensor-core (DMMA) kernel
 cudaError_t launch_tet_stage(int N, const StageParams& p, cudaStream_t s);
+cudaError_t launch_wedge_wadg_stage(int N, const StageParams& p, cudaStream_t s); // WADG (DMMA) kernel
+/// Mtilde-norm wedge energy partials, one per block of wadg_energy_elems_per_block() wedges
+cudaError_t launch_wadg_energy(int N, const EnergyParams& p, int* nblocks_out, cudaStream_t s);
 int wedge_elems_per_block(int N);
 int tet_elems_per_block(int N);
 cudaError_t launch_energy(int N, const EnergyParams& p, int* nblocks_out, cudaStream_t s);

@@ -94,7 +94,9 @@ Discretization build_discretization(HybridMesh mesh, int degree, FluxConfig flux
   d.wgeo.resize(nw);
   d.txJ.resize((std::size_t)nw * nq);
   d.tyJ.resize((std::size_t)nw * nq);
-  const bool need_L = mass_mode != MassMode::wadg || true; // the oracle / exact path use L
+  // WADG needs no per-wedge operator storage; the stored lifts are kept only
+  // when asked for (the CPU oracle restates WADG through the exact lifts)
+  const bool need_L = mass_mode != MassMode::wadg || with_quad_lift;
   if (need_L) d.tri_lift.resize((std::size_t)nw * nt * nt);
   if (with_quad_lift) d.quad_lift.resize((std::size_t)nw * 3 * nq * nt);
   d.tgeo.resize(ntet);
@@ -126,10 +128,16 @@ Discretization build_discretization(HybridMesh mesh, int degree, FluxConfig flux
         d.txJ[(std::size_t)w * nq + j] = g.txJ[j];
         d.tyJ[(std::size_t)w * nq + j] = g.tyJ[j];
       }
-      if (!wedge_lifts_flat(g.j0, g.j_r, g.j_s, o.jf_quad, d.refs,
-                            d.tri_lift.data() + (std::size_t)w * nt * nt,
-                            with_quad_lift ? d.quad_lift.data() + (std::size_t)w * 3 * nq * nt : nullptr))
-        throw NumericalError("weighted triangle mass matrix is not SPD");
+      if (need_L) {
+        if (!wedge_lifts_flat(g.j0, g.j_r, g.j_s, o.jf_quad, d.refs,
+                              d.tri_lift.data() + (std::size_t)w * nt * nt,
+                              with_quad_lift ? d.quad_lift.data() + (std::size_t)w * 3 * nq * nt : nullptr))
+          throw NumericalError("weighted triangle mass matrix is not SPD");
+      } else if (!(g.j0 - g.j_r - g.j_s > 0.0 && g.j0 + g.j_r - g.j_s > 0.0 && g.j0 - g.j_r + g.j_s > 0.0)) {
+        // J is affine in (r, s): positive at the triangle vertices (-1,-1),
+        // (1,-1), (-1,1) means positive everywhere, so M_{1/J} is SPD
+        throw NumericalError("wedge Jacobian is not positive");
+      }
     } catch (const std::exception& ex) {
 #pragma omp critical
       if (bad_wedge < 0 || w < bad_wedge) {

@@ -222,6 +222,52 @@ void apply_tet_mass(const ElementGeometry& g, const References& refs, const Vec&
   for (double& v : out) v *= g.j0;
 }
 
+Mat wedge_inv_j_mass(double j0, double jr, double js, const References& refs) {
+  const auto& tri = refs.tri;
+  const int nt = tri.num_nodes, nc = (int)tri.cubature.weights.size();
+  Mat out(nt, nt);
+  for (int q = 0; q < nc; ++q) {
+    const double J = j0 + jr * tri.cubature.points(q, 0) + js * tri.cubature.points(q, 1);
+    const double wq = tri.cubature.weights[q] / J;
+    for (int a = 0; a < nt; ++a)
+      for (int b = 0; b < nt; ++b) out(a, b) += tri.interp_cub(q, a) * wq * tri.interp_cub(q, b);
+  }
+  return out;
+}
+
+WadgTables build_wadg_tables(const References& refs) {
+  const auto& tri = refs.tri;
+  WadgTables w;
+  w.nt = tri.num_nodes;
+  w.nq = refs.degree + 1;
+  w.nc = (int)tri.cubature.weights.size();
+  w.inv_mass = inverse(tri.mass);
+  w.Kr = matmul(w.inv_mass, tri.moment_r);
+  w.Ks = matmul(w.inv_mass, tri.moment_s);
+  w.kd[0] = tri.dr;
+  w.kd[1] = matmul(w.Kr, tri.dr);
+  w.kd[2] = matmul(w.Ks, tri.dr);
+  w.kd[3] = tri.ds;
+  w.kd[4] = matmul(w.Kr, tri.ds);
+  w.kd[5] = matmul(w.Ks, tri.ds);
+  Mat vw = transpose(tri.interp_cub); // nt x nc
+  for (int a = 0; a < w.nt; ++a)
+    for (int q = 0; q < w.nc; ++q) vw(a, q) *= tri.cubature.weights[q];
+  w.Pw = matmul(w.inv_mass, vw);
+  w.Vq = tri.interp_cub;
+  w.qr.resize(w.nc);
+  w.qs.resize(w.nc);
+  for (int q = 0; q < w.nc; ++q) {
+    w.qr[q] = tri.cubature.points(q, 0);
+    w.qs[q] = tri.cubature.points(q, 1);
+  }
+  for (int e = 0; e < 3; ++e) {
+    w.R0[e] = matmul(w.inv_mass, wedge_edge_mass_embedded(e, 1.0, 0.0, refs));
+    w.R1[e] = matmul(w.inv_mass, wedge_edge_mass_embedded(e, 0.0, 1.0, refs));
+  }
+  return w;
+}
+
 StorageReport storage_report(int degree, const std::vector<WedgeOperators>& wedges,
                              const std::vector<TetOperators>& tets) {
   StorageReport rep;

@@ -249,10 +249,13 @@ class Discretization:
 
 
 def build_discretization(mesh: HybridMesh, degree: int, flux="upwind", tau_p=0.0, tau_u=0.0,
-                         mass="exact", threads=0) -> Discretization:
+                         mass="exact", threads=0, host_lifts=True) -> Discretization:
+    """build_discretization (solver.hpp:61-63).  mass: "exact" | "lumped" | "wadg".
+    host_lifts=False (wadg only) skips the per-wedge exact lifts on the host too."""
     out = C.c_void_p()
-    check(lib().pdg_disc_build(mesh.handle, degree, capi.FLUX[flux], tau_p, tau_u, capi.MASS[mass],
-                               threads, C.byref(out)))
+    flags = 0 if host_lifts else 1  # PDG_DISC_NO_HOST_LIFTS
+    check(lib().pdg_disc_build_ex(mesh.handle, degree, capi.FLUX[flux], tau_p, tau_u, capi.MASS[mass],
+                                  threads, flags, C.byref(out)))
     return Discretization(out.value, mesh)
 
 
