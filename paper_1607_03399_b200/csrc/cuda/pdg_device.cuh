@@ -119,6 +119,7 @@ struct StageParams {
   unsigned long long* ticket;
   unsigned long long ticket_base;
   unsigned long long* ticket_host_next; // host side: next base (advanced by the launcher)
+  int ticket_batch;                     // consecutive elements per ticket (set by the launcher)
 };
 
 struct EnergyParams {

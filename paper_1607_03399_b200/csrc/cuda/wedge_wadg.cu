@@ -84,6 +84,17 @@ struct WCfg {
   static_assert(SMEM_BYTES <= 227 * 1024, "WADG tables do not fit in shared memory");
 };
 
+/// elements per ticket: batching cuts same-address atomics (the global work
+/// counter) at low N, where an element is only a few hundred cycles of work
+inline int ticket_batch(int N) {
+  static const int env = [] {
+    const char* v = std::getenv("PDG_TICKET_BATCH");
+    return v ? std::atoi(v) : 0;
+  }();
+  if (env > 0) return env;
+  return N <= 3 ? 8 : 2; // measured sweep, round 1 (profiles/round1_ticket_batch.txt)
+}
+
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d[0]), "+d"(d[1])
@@ -216,7 +227,17 @@ __global__ void __launch_bounds__(WCfg<N, NST>::THREADS, 1) wedge_wadg_kernel(co
   const bool first = mode & M_FIRST, accum = !FUSED && (mode & M_ACCUM);
   const double* res_src = lserk ? (first ? nullptr : p.res) : (accum ? p.rhs_out : nullptr);
   volatile long long* slot = reinterpret_cast<volatile long long*>(bar + 2);
-  auto grab = [&]() -> long long { return (long long)(atomicAdd(p.ticket, 1ULL) - p.ticket_base); };
+  // tickets hand out batches of B consecutive elements (thread 0 of the team
+  // keeps the current batch); one failing grab per team ends its loop
+  const int B = p.ticket_batch;
+  long long bnext = 0, bend = 0;
+  auto grab = [&]() -> long long {
+    if (bnext >= bend) {
+      bnext = (long long)(atomicAdd(p.ticket, (unsigned long long)B) - p.ticket_base);
+      bend = bnext + B < p.Kw_active ? bnext + B : (bnext < p.Kw_active ? p.Kw_active : bnext + 1);
+    }
+    return bnext++;
+  };
   if (tt == 0) {
     const long long e0 = grab();
     slot[0] = e0;
@@ -508,7 +529,9 @@ cudaError_t launch_wadg_NC(const StageParams& p, cudaStream_t s) {
   const int grid = (int)(need < grid_cap ? need : grid_cap);
   StageParams q = p;
   q.ticket_base = *p.ticket_host_next;
-  *p.ticket_host_next += (unsigned long long)p.Kw_active + (unsigned long long)grid * C::TPB;
+  q.ticket_batch = ticket_batch(N);
+  const unsigned long long B = (unsigned long long)q.ticket_batch;
+  *p.ticket_host_next += B * (((unsigned long long)p.Kw_active + B - 1) / B + (unsigned long long)grid * C::TPB);
   kern<<<grid, C::THREADS, C::SMEM_BYTES, s>>>(q);
   return cudaGetLastError();
 }
