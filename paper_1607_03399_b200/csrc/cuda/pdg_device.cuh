@@ -141,6 +141,8 @@ struct EnergyParams {
 // launchers (instantiated per degree in the .cu files)
 cudaError_t launch_wedge_stage(int N, const StageParams& p, cudaStream_t s); // FP64 tensor-core (DMMA) kernel
 cudaError_t launch_tet_stage(int N, const StageParams& p, cudaStream_t s);
+bool tet_dmma_supported(int N);
+cudaError_t launch_tet_dmma_stage(int N, const StageParams& p, cudaStream_t s); // batched DMMA tet kernel (N <= 5)
 cudaError_t launch_wedge_wadg_stage(int N, const StageParams& p, cudaStream_t s); // WADG (DMMA) kernel
 /// Mtilde-norm wedge energy partials, one per block of wadg_energy_elems_per_block() wedges
 cudaError_t launch_wadg_energy(int N, const EnergyParams& p, int* nblocks_out, cudaStream_t s);

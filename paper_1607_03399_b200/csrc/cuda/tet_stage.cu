@@ -1,4 +1,5 @@
-// Fused tetrahedron stage kernel: volume + surface + media + LSERK45 update.
+// Fused tetrahedron stage kernel (CUDA cores): volume + surface + media + LSERK45
+// update.  Used for N = 6..9; N <= 5 dispatches to the DMMA kernel (tet_dmma.cu).
 //
 // One CTA handles E tets, one thread per volume node.  Tets are affine, so the
 // physical derivative rows are c_x(n,k) = rx Dr(n,k) + sx Ds(n,k) + tx Dt(n,k)
@@ -7,6 +8,8 @@
 // Reference: tet_volume_elem / surface_elem (tet branch) / scale_media
 // (proj/src/solver.cpp:220-254, 321-333, 337-346).
 #include <cuda_runtime.h>
+
+#include <cstdlib>
 
 #include "pdg_device.cuh"
 
@@ -196,6 +199,14 @@ int tet_elems_per_block(int N) {
 }
 
 cudaError_t launch_tet_stage(int N, const StageParams& p, cudaStream_t s) {
+  // N <= 5: batched tensor-core kernel (tet_dmma.cu); the thread-per-node
+  // CUDA-core kernel below covers N = 6..9 (operators too large for shared
+  // memory) and PDG_TET_KERNEL=simt
+  static const bool simt = [] {
+    const char* v = std::getenv("PDG_TET_KERNEL");
+    return v && v[0] == 's';
+  }();
+  if (!simt && tet_dmma_supported(N)) return launch_tet_dmma_stage(N, p, s);
   switch (N) {
 #define PDG_CASE(n) case n: return launch_tet_N<n>(p, s);
     PDG_CASE(1) PDG_CASE(2) PDG_CASE(3) PDG_CASE(4) PDG_CASE(5) PDG_CASE(6) PDG_CASE(7)
