@@ -12,6 +12,8 @@ import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libprismdg_b200.so")
+# development only: load an alternative in-tree build (kernel configuration sweeps)
+LIB_PATH = os.environ.get("PDG_LIB_PATH", LIB_PATH)
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "prismdg_b200.h")
 
 PDG_OK = 0

@@ -139,7 +139,9 @@ void launch_checked(pdg_ctx* c, const StageParams& p, bool wedge) {
     PDG_CK(cudaEventRecord(a, c->stream));
   }
   cudaError_t err = !wedge ? launch_tet_stage(c->N, p, c->stream)
-                    : (c->wadg ? launch_wedge_wadg_stage(c->N, p, c->stream) : launch_wedge_stage(c->N, p, c->stream));
+                    : c->wadg ? launch_wedge_wadg_stage(c->N, p, c->stream)
+                    : c->wedge_simt ? launch_wedge_simt_stage(c->N, p, c->stream)
+                                    : launch_wedge_stage(c->N, p, c->stream);
   if (err != cudaSuccess) throw DeviceError(std::string("stage kernel launch failed: ") + cudaGetErrorString(err));
   if (c->flags & 2) {
     PDG_CK(cudaEventRecord(b, c->stream));
@@ -380,9 +382,22 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags,
       } else {
         std::vector<long long> word0(word);
         if (c->Kw > 0 && d.quad_lift.empty()) throw prismdg::ConfigError("device path needs the quad lifts");
-        c->Lt = dalloc<double>((std::size_t)c->Kw * lfrag_of(N));
-        c->QL = dalloc<double>((std::size_t)c->Kw * qfrag_of(N));
-        upload_wedge_fragments(c, d, word0);
+        static const bool force_dmma = [] {
+          const char* v = std::getenv("PDG_WEDGE_KERNEL");
+          return v && v[0] == 'd';
+        }();
+        c->wedge_simt = !force_dmma && N <= wedge_simt_max_degree();
+        if (c->wedge_simt) {
+          // compact host layouts, no fragment padding: L [k][i], quad lifts [f][a][i]
+          c->Lt = dalloc<double>((std::size_t)c->Kw * nt * nt);
+          c->QL = dalloc<double>((std::size_t)c->Kw * 3 * nq * nt);
+          upload_permuted(c->Lt, d.tri_lift.data(), (std::size_t)nt * nt, word0);
+          upload_permuted(c->QL, d.quad_lift.data(), (std::size_t)3 * nq * nt, word0);
+        } else {
+          c->Lt = dalloc<double>((std::size_t)c->Kw * lfrag_of(N));
+          c->QL = dalloc<double>((std::size_t)c->Kw * qfrag_of(N));
+          upload_wedge_fragments(c, d, word0);
+        }
       }
     }
 

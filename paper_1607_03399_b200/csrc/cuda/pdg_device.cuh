@@ -142,6 +142,8 @@ struct EnergyParams {
 cudaError_t launch_wedge_stage(int N, const StageParams& p, cudaStream_t s); // FP64 tensor-core (DMMA) kernel
 cudaError_t launch_tet_stage(int N, const StageParams& p, cudaStream_t s);
 bool tet_dmma_supported(int N);
+int wedge_simt_max_degree();
+cudaError_t launch_wedge_simt_stage(int N, const StageParams& p, cudaStream_t s); // low-order CUDA-core wedge kernel
 cudaError_t launch_tet_dmma_stage(int N, const StageParams& p, cudaStream_t s); // batched DMMA tet kernel (N <= 5)
 cudaError_t launch_wedge_wadg_stage(int N, const StageParams& p, cudaStream_t s); // WADG (DMMA) kernel
 /// Mtilde-norm wedge energy partials, one per block of wadg_energy_elems_per_block() wedges

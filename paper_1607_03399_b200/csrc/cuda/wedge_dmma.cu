@@ -55,6 +55,9 @@ constexpr int kComboCap = 4096; // ints of neighbour node maps kept in shared me
 #define PDG_WEDGE_STAGES 2
 #endif
 constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1 or 2)
+#ifndef PDG_THREAD_CAP
+#define PDG_THREAD_CAP 512
+#endif
 
 template <int N, int NST_>
 struct DCfg {
@@ -80,8 +83,8 @@ struct DCfg {
   static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 2 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
   static constexpr int PER_TEAM = 4 + NSTAGE * STAGE + WORK;
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
-  // <= 512 threads per CTA keeps >= 128 registers per thread
-  static constexpr int TPB = cmax(1, cmin(cmin(15, 512 / (32 * T)), TPB_SMEM)); // teams per CTA
+  // <= PDG_THREAD_CAP threads per CTA (512 keeps >= 128 registers per thread)
+  static constexpr int TPB = cmax(1, cmin(cmin(15, PDG_THREAD_CAP / (32 * T)), TPB_SMEM)); // teams per CTA
   static constexpr int THREADS = 32 * T * TPB;
   static constexpr size_t SMEM_BYTES = (size_t)8 * (TABLES + TPB * PER_TEAM);
   static constexpr int QF_LANE = ceil_div(FW, 32 * T); // face nodes per team thread

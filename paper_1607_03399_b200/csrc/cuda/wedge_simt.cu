@@ -1,0 +1,448 @@
+// Fused wedge stage kernel for low orders (N <= 3), FP64 CUDA cores.
+//
+// At N = 1..3 a wedge is 24..160 DOFs and its triangle matrices are 3x3..10x10:
+// an 8x8x4 tensor-core tile is mostly padding (9% useful at N=1) and a team of
+// warps per wedge leaves the SM waiting on one element's latency chain.  Here
+// one thread owns one (wedge, triangle node i) pair and every slice j of it,
+// so a 128-thread CTA works on E = 128 / NT wedges at once (42 at N=1) and the
+// per-element products are short register-resident dot products:
+//   V(j,i)  = -(txJ_j Dt UX + tyJ_j Dt UY + tzJ Dt UZ)(j,i) + tri-face p lifts
+//   gx, gy  = (rx Dr + sx Ds) P, (ry Dr + sy Ds) P          (row i)
+//   dv      = (rx Dr + sx Ds) UX + (ry Dr + sy Ds) UY
+//   LP, L Fu_bottom, L Fu_top, LV  with the row L(i, :) held in registers
+//   LY      = LP Dt^T; quad-face lifts QL_f(i, :) [Fp_f | Fu_f]
+// then media scaling and the LSERK45 stage, written straight to HBM.
+// Same algebra and operation order per output as the DMMA kernel
+// (wedge_dmma.cu), i.e. the reference's wedge_volume_elem / surface_elem /
+// scale_media / lserk (proj/src/solver.cpp:164-218, 258-335, 337-346, 541-551)
+// with the lift folds of SURVEY.md A.3.
+//
+// Data movement: the state, record and connectivity of the next chunk of E
+// wedges are copied global -> shared with cp.async (16-byte LDGSTS) into
+// per-element slots whose strides are chosen to spread the shared-memory
+// banks, double-buffered against the current chunk's work; L^{tri,k} and the
+// quad lifts (compact [k][i] / [f][a][i] layouts: no padding bytes) and the
+// residual are read per thread from HBM into registers; neighbour traces are
+// L2 gathers (chunks are handed out by a global ticket, so CTAs work on a
+// narrow window of the Morton-ordered element list).
+#include <cuda_runtime.h>
+
+#include "pdg_device.cuh"
+
+namespace pdg {
+
+namespace {
+
+__host__ __device__ constexpr int r2(int x) { return (x + 1) & ~1; }
+
+/// wavefronts a warp needs to read doubles at addresses {e*S + i}, lane = e*NT + i
+/// (16 eight-byte bank pairs, distinct addresses on one pair serialise)
+__host__ __device__ constexpr int conflict_degree(int S, int NT) {
+  int worst = 0;
+  for (int b = 0; b < 16; ++b) {
+    int cnt = 0;
+    for (int lane = 0; lane < 32; ++lane) {
+      const int e = lane / NT, i = lane - e * NT;
+      if (((e * S + i) & 15) == b) ++cnt;
+    }
+    worst = cnt > worst ? cnt : worst;
+  }
+  return worst;
+}
+/// smallest even stride >= x with the least bank conflicts for the {e*S + i} pattern
+__host__ __device__ constexpr int slot_stride(int x, int NT) {
+  int best = r2(x), bd = conflict_degree(r2(x), NT);
+  for (int s = r2(x) + 2; s < r2(x) + 16; s += 2) {
+    const int d = conflict_degree(s, NT);
+    if (d < bd) {
+      bd = d;
+      best = s;
+    }
+  }
+  return best;
+}
+
+#ifndef PDG_SIMT_THREADS
+#define PDG_SIMT_THREADS 128
+#endif
+#ifndef PDG_SIMT_MINB
+#define PDG_SIMT_MINB 1
+#endif
+
+template <int N>
+struct SCfg {
+  static constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npw_of(N), FW = fw_of(N), WG = wg_of(N);
+  static constexpr int THREADS = PDG_SIMT_THREADS;
+  static constexpr int E = THREADS / NT;      // wedges per chunk
+  static constexpr int ACT = E * NT;          // threads with a (wedge, node) pair
+  static constexpr int SU = slot_stride(4 * NP, NT);
+  static constexpr int SG = slot_stride(WG + kWC / 2, NT); // record + connectivity
+  static constexpr int STAGE = E * (SU + SG);
+  static constexpr int FT = 4 * NT;                   // tri fluxes: [p|u][bottom|top][NT]
+  static constexpr int FQ = 6 * NQ * NQ;              // quad fluxes: [p|u][face][a][j]
+  static constexpr int SF = slot_stride(FT + FQ, NT);
+  static constexpr int SV = slot_stride(NQ * NT, NT); // V(j, i) at j*NT + i
+  static constexpr int TABLES = r2(r2(2 * NT * NT + NQ * NQ + 2 * NQ) + ceil_div(FW, 2) + 2048 / 2);
+  static constexpr size_t SMEM_BYTES = (size_t)8 * (TABLES + 2 * STAGE + E * (SF + SV) + 4);
+  static constexpr int TASKS = ceil_div(E * FW, THREADS);
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(K) : "memory");
+}
+
+/// copy the state, record and connectivity of wedges [e0, e0+nel) into stage slots
+template <int N>
+__device__ __forceinline__ void load_chunk(const StageParams& p, double* stg, long long e0, int nel) {
+  using C = SCfg<N>;
+  constexpr int UV = 4 * C::NP / 2;     // 16-byte vectors per state block
+  constexpr int GV = C::WG / 2;         // per record
+  constexpr int CV = kWC / 4;           // per connectivity record (ints)
+  double* sU = stg;
+  double* sG = stg + C::E * C::SU;
+  for (int q = threadIdx.x; q < nel * UV; q += C::THREADS) {
+    const int e = q / UV, v = q - e * UV;
+    cp_async16(sU + e * C::SU + 2 * v, p.u_in + (e0 + e) * 4 * C::NP + 2 * v);
+  }
+  for (int q = threadIdx.x; q < nel * (GV + CV); q += C::THREADS) {
+    const int e = q / (GV + CV), v = q - e * (GV + CV);
+    if (v < GV)
+      cp_async16(sG + e * C::SG + 2 * v, p.wgeo + (e0 + e) * C::WG + 2 * v);
+    else
+      cp_async16(sG + e * C::SG + C::WG + 2 * (v - GV), p.wconn + (e0 + e) * kWC + 4 * (v - GV));
+  }
+}
+
+template <int N>
+__global__ void __launch_bounds__(SCfg<N>::THREADS, PDG_SIMT_MINB) wedge_simt_kernel(const StageParams p) {
+  using C = SCfg<N>;
+  constexpr int NQ = C::NQ, NT = C::NT, NP = C::NP, FW = C::FW, WG = C::WG, E = C::E;
+  constexpr int SU = C::SU, SG = C::SG, SF = C::SF, SV = C::SV;
+  extern __shared__ __align__(16) double smem[];
+  double* sDrT = smem;                 // [k][i]
+  double* sDsT = sDrT + NT * NT;       // [k][i]
+  double* sDt = sDsT + NT * NT;        // [j][l]
+  double* sProf = sDt + NQ * NQ;       // [2][NQ]
+  int* sWface = reinterpret_cast<int*>(smem + r2(2 * NT * NT + NQ * NQ + 2 * NQ));
+  int* sCombo = sWface + 2 * ceil_div(FW, 2);
+  double* stg = smem + C::TABLES;      // 2 stages
+  double* sF = stg + 2 * C::STAGE;     // per wedge fluxes
+  double* sV = sF + E * SF;            // per wedge V
+  volatile long long* slot = reinterpret_cast<volatile long long*>(sV + E * SV);
+  for (int q = threadIdx.x; q < NT * NT; q += C::THREADS) {
+    sDrT[q] = p.DrT[q];
+    sDsT[q] = p.DsT[q];
+  }
+  for (int q = threadIdx.x; q < NQ * NQ; q += C::THREADS) sDt[q] = p.Dt[q];
+  for (int q = threadIdx.x; q < 2 * NQ; q += C::THREADS) sProf[q] = p.prof[q];
+  for (int q = threadIdx.x; q < FW; q += C::THREADS) sWface[q] = p.wface_dev[q];
+  const bool combo_smem = p.nbr_nodes_len <= 2048;
+  if (combo_smem)
+    for (int q = threadIdx.x; q < p.nbr_nodes_len; q += C::THREADS) sCombo[q] = p.nbr_nodes[q];
+  const int* combo = combo_smem ? sCombo : p.nbr_nodes;
+
+  const int mode = p.mode;
+  const bool vol = mode & M_VOLUME, surf = mode & M_SURFACE;
+  const bool lserk = mode & M_LSERK, media = mode & M_MEDIA;
+  const bool first = mode & M_FIRST, accum = mode & M_ACCUM;
+  const double* res_src = lserk ? (first ? nullptr : p.res) : (accum ? p.rhs_out : nullptr);
+  const long long nchunk = (p.Kw_active + E - 1) / E;
+  auto nel_of = [&](long long c) -> int {
+    const long long r = p.Kw_active - c * E;
+    return (int)(r < E ? r : E);
+  };
+  if (threadIdx.x == 0) {
+    slot[0] = (long long)(atomicAdd(p.ticket, 1ULL) - p.ticket_base);
+    slot[1] = (long long)(atomicAdd(p.ticket, 1ULL) - p.ticket_base);
+  }
+  __syncthreads();
+  long long c = slot[0], cn = slot[1];
+  if (c < nchunk) load_chunk<N>(p, stg, c * E, nel_of(c));
+  cp_async_commit();
+
+  const int el = threadIdx.x / NT, i = threadIdx.x - el * NT; // this thread's (wedge, node)
+  for (int it = 0; c < nchunk; ++it) {
+    double* cur = stg + (it & 1) * C::STAGE;
+    // prefetch the next chunk into the other stage (it was released by the
+    // trailing barrier of the previous iteration)
+    if (cn < nchunk) load_chunk<N>(p, stg + ((it + 1) & 1) * C::STAGE, cn * E, nel_of(cn));
+    cp_async_commit();
+    cp_async_wait<1>();
+    // next ticket; the slot alternates with the iteration parity so it is never
+    // rewritten before every thread has read it
+    if (threadIdx.x == 0) slot[2 + (it & 1)] = (long long)(atomicAdd(p.ticket, 1ULL) - p.ticket_base);
+    __syncthreads();
+    const long long e0 = c * E;
+    const int nel = nel_of(c);
+    const double* sU = cur;
+    const double* sG = cur + E * SU;
+    const bool active = threadIdx.x < C::ACT && el < nel;
+    const double* U = sU + el * SU;
+    const double* G = sG + el * SG;
+    const long long ge = e0 + el;
+
+    // per-thread operands from HBM: row i of L, rows i of the quad lifts, residual
+    double Lr[NT], rres[4][NQ];
+    if (active) {
+      const double* L = p.Lt + ge * NT * NT + i;
+#pragma unroll
+      for (int k = 0; k < NT; ++k) Lr[k] = __ldcs(L + k * NT);
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int j = 0; j < NQ; ++j)
+          rres[f][j] = res_src ? __ldcs(res_src + ge * 4 * NP + f * NP + j * NT + i) : 0.0;
+    }
+
+    // ---- numerical fluxes of the chunk -------------------------------------------
+    if (surf) {
+      double nbv[C::TASKS][4];
+#pragma unroll
+      for (int q = 0; q < C::TASKS; ++q) {
+        const int m = threadIdx.x + C::THREADS * q;
+        if (m < nel * FW) {
+          const int e = m / FW, fm = m - e * FW;
+          const int f = fm < NT ? 0 : (fm < 2 * NT ? 1 : 2 + (fm - 2 * NT) / (NQ * NQ));
+          const int loc = fm < 2 * NT ? fm - f * NT : (fm - 2 * NT) - (f - 2) * NQ * NQ;
+          const int* Cn = reinterpret_cast<const int*>(sG + e * SG + WG);
+          const int nbr = Cn[2 * f];
+          if (nbr >= 0) {
+            const int node = combo[Cn[2 * f + 1] * p.max_nfp + loc];
+            const double* src;
+            int fs;
+            if (nbr < p.Kw) {
+              src = p.u_in + (long long)nbr * 4 * NP + node;
+              fs = NP;
+            } else {
+              src = p.u_in + p.tet_base + (long long)(nbr - p.Kw) * 4 * npt_of(N) + node;
+              fs = npt_of(N);
+            }
+            nbv[q][0] = __ldg(src);
+            nbv[q][1] = __ldg(src + fs);
+            nbv[q][2] = __ldg(src + 2 * fs);
+            nbv[q][3] = __ldg(src + 3 * fs);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < C::TASKS; ++q) {
+        const int m = threadIdx.x + C::THREADS * q;
+        if (m < nel * FW) {
+          const int e = m / FW, fm = m - e * FW;
+          const int f = fm < NT ? 0 : (fm < 2 * NT ? 1 : 2 + (fm - 2 * NT) / (NQ * NQ));
+          const int loc = fm < 2 * NT ? fm - f * NT : (fm - 2 * NT) - (f - 2) * NQ * NQ;
+          const double* Ue = sU + e * SU;
+          const double* Ge = sG + e * SG;
+          const int* Cn = reinterpret_cast<const int*>(Ge + WG);
+          const int my = sWface[fm];
+          const double pm = Ue[my];
+          const double nx = Ge[w_nrm(N) + 3 * f], ny = Ge[w_nrm(N) + 3 * f + 1], nz = Ge[w_nrm(N) + 3 * f + 2];
+          const double taup = Ge[w_taup(N) + f], tauu = Ge[w_tauu(N) + f];
+          double fp, fu;
+          if (Cn[2 * f] >= 0) {
+            const double dp = nbv[q][0] - pm;
+            const double dun = nx * (nbv[q][1] - Ue[NP + my]) + ny * (nbv[q][2] - Ue[2 * NP + my]) +
+                               nz * (nbv[q][3] - Ue[3 * NP + my]);
+            fp = 0.5 * (taup * dp - dun);
+            fu = 0.5 * (tauu * dun - dp);
+          } else {
+            const double dp = -2.0 * pm; // reflective: p+ = -p-, u+ = u-
+            fp = 0.5 * taup * dp;
+            fu = -0.5 * dp;
+          }
+          double* Fe = sF + e * SF;
+          if (f < 2) {
+            Fe[f * NT + loc] = fp;            // Ftp[f][loc]
+            Fe[2 * NT + f * NT + loc] = fu;   // Ftu[f][loc]
+          } else {
+            Fe[4 * NT + (f - 2) * NQ * NQ + loc] = fp;            // Fqp[f-2][a][j]
+            Fe[4 * NT + 3 * NQ * NQ + (f - 2) * NQ * NQ + loc] = fu; // Fqu
+          }
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- V column i, gradients, L products, quad lifts -------------------------------
+    double rp[NQ], rux[NQ], ruy[NQ], ruz[NQ], lp[NQ];
+    double lf0 = 0.0, lf1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) rp[j] = rux[j] = ruy[j] = ruz[j] = lp[j] = 0.0;
+    if (active) {
+      const double* Fe = sF + el * SF;
+      const double tzJ = G[W_TZJ], jfb = G[W_JFB], jft = G[W_JFT];
+      {
+        const double fb = surf ? jfb * Fe[i] : 0.0, ftop = surf ? jft * Fe[NT + i] : 0.0;
+        double* Ve = sV + el * SV;
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) {
+          double d = 0.0;
+          if (vol) {
+            const double sx_ = G[W_TXJ + j], sy_ = G[w_tyj(N) + j];
+#pragma unroll
+            for (int l = 0; l < NQ; ++l) {
+              const double dt = sDt[j * NQ + l];
+              d += U[NP + l * NT + i] * (sx_ * dt);
+              d += U[2 * NP + l * NT + i] * (sy_ * dt);
+              d += U[3 * NP + l * NT + i] * (tzJ * dt);
+            }
+          }
+          Ve[j * NT + i] = -d + fb * sProf[j] + ftop * sProf[NQ + j];
+        }
+      }
+      const double rx = G[W_RX], ry = G[W_RY], sxm = G[W_SX], sym = G[W_SY];
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        const double lk = Lr[k];
+        double cx = 0.0, cy = 0.0;
+        if (vol) {
+          const double dr = sDrT[k * NT + i], ds = sDsT[k * NT + i];
+          cx = rx * dr + sxm * ds;
+          cy = ry * dr + sym * ds;
+        }
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) {
+          const double pk = U[j * NT + k];
+          lp[j] += lk * pk;
+          if (vol) {
+            rux[j] -= cx * pk;
+            ruy[j] -= cy * pk;
+            rp[j] -= cx * U[NP + j * NT + k] + cy * U[2 * NP + j * NT + k];
+          }
+        }
+        if (surf) {
+          lf0 += lk * Fe[2 * NT + k];
+          lf1 += lk * Fe[3 * NT + k];
+        }
+      }
+      if (surf) {
+        const double* QL = p.QL + ge * 3 * NQ * NT + i;
+        const double* nrm = G + w_nrm(N);
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          double qu[NQ];
+#pragma unroll
+          for (int j = 0; j < NQ; ++j) qu[j] = 0.0;
+#pragma unroll
+          for (int a = 0; a < NQ; ++a) {
+            const double q = __ldcs(QL + (f * NQ + a) * NT);
+#pragma unroll
+            for (int j = 0; j < NQ; ++j) {
+              rp[j] += q * Fe[4 * NT + (f * NQ + a) * NQ + j];
+              qu[j] += q * Fe[4 * NT + 3 * NQ * NQ + (f * NQ + a) * NQ + j];
+            }
+          }
+          const double nx = nrm[3 * (f + 2)], ny = nrm[3 * (f + 2) + 1], nz = nrm[3 * (f + 2) + 2];
+#pragma unroll
+          for (int j = 0; j < NQ; ++j) {
+            rux[j] += nx * qu[j];
+            ruy[j] += ny * qu[j];
+            ruz[j] += nz * qu[j];
+          }
+        }
+      }
+    }
+    __syncthreads(); // V complete
+
+    // ---- L V, L Y, tri-face velocity lifts, media, LSERK -----------------------------
+    if (active) {
+      const double* Ve = sV + el * SV;
+      const double tzJ = G[W_TZJ], jfb = G[W_JFB], jft = G[W_JFT];
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        const double lk = Lr[k];
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) rp[j] += lk * Ve[j * NT + k];
+      }
+      const double* nrm = G + w_nrm(N);
+      const double kappa = G[W_KAPPA], irho = G[W_IRHO];
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) {
+        if (vol) {
+          double ly = 0.0;
+#pragma unroll
+          for (int l = 0; l < NQ; ++l) ly += lp[l] * sDt[j * NQ + l];
+          rux[j] -= G[W_TXJ + j] * ly;
+          ruy[j] -= G[w_tyj(N) + j] * ly;
+          ruz[j] -= tzJ * ly;
+        }
+        if (surf) {
+          const double t0 = jfb * sProf[j] * lf0, t1 = jft * sProf[NQ + j] * lf1;
+          rux[j] += nrm[0] * t0 + nrm[3] * t1;
+          ruy[j] += nrm[1] * t0 + nrm[4] * t1;
+          ruz[j] += nrm[2] * t0 + nrm[5] * t1;
+        }
+        if (media) {
+          rp[j] *= kappa;
+          rux[j] *= irho;
+          ruy[j] *= irho;
+          ruz[j] *= irho;
+        }
+        const double rv[4] = {rp[j], rux[j], ruy[j], ruz[j]};
+#pragma unroll
+        for (int f = 0; f < 4; ++f) {
+          const int o = f * NP + j * NT + i;
+          const long long go = ge * 4 * NP + o;
+          if (lserk) {
+            const double rr = first ? p.dt * rv[f] : p.a * rres[f][j] + p.dt * rv[f];
+            __stcs(p.res + go, rr);
+            __stcs(p.u_out + go, U[o] + p.b * rr);
+          } else {
+            __stcs(p.rhs_out + go, accum ? rres[f][j] + rv[f] : rv[f]);
+          }
+        }
+      }
+    }
+    __syncthreads(); // the stage and the work buffers are free again
+    c = cn;
+    cn = slot[2 + (it & 1)];
+  }
+  cp_async_wait<0>();
+}
+
+template <int N>
+cudaError_t launch_simt_N(const StageParams& p, cudaStream_t s) {
+  using C = SCfg<N>;
+  static int grid_cap = 0;
+  auto kern = wedge_simt_kernel<N>;
+  if (grid_cap == 0) {
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
+    if (err != cudaSuccess) return err;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM_BYTES);
+    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  if (p.Kw_active == 0) return cudaSuccess;
+  const long long nchunk = (p.Kw_active + C::E - 1) / C::E;
+  const int grid = (int)(nchunk < grid_cap ? nchunk : grid_cap);
+  StageParams q = p;
+  q.ticket_base = *p.ticket_host_next;
+  // every CTA grabs until it gets two tickets past the end (one in flight)
+  *p.ticket_host_next += (unsigned long long)nchunk + 2ull * (unsigned long long)grid;
+  kern<<<grid, C::THREADS, C::SMEM_BYTES, s>>>(q);
+  return cudaGetLastError();
+}
+
+} // namespace
+
+int wedge_simt_max_degree() { return 3; }
+
+cudaError_t launch_wedge_simt_stage(int N, const StageParams& p, cudaStream_t s) {
+  switch (N) {
+    case 1: return launch_simt_N<1>(p, s);
+    case 2: return launch_simt_N<2>(p, s);
+    case 3: return launch_simt_N<3>(p, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+} // namespace pdg
