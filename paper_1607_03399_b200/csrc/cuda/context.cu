@@ -161,6 +161,7 @@ StageParams base_params(pdg_ctx* c) {
   p.Lt = c->Lt;
   p.QL = c->QL;
   p.wadg = c->wadg;
+  p.wadg_frag = c->wadg_frag;
   p.tgeo = c->tgeo;
   p.tconn = c->tconn;
   p.DrT = c->DrT;
@@ -379,6 +380,8 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags,
         // reduced storage: shared tables only, nothing per wedge beyond the record
         if (N > 7) throw prismdg::ConfigError("the WADG device path supports degrees 1..7");
         c->wadg = upload(flatten_wadg(d));
+        c->wadg_frag = dalloc<double>(wadg_frag_size(N));
+        PDG_CK(launch_wadg_frag_fill(N, c->wadg, c->wadg_frag, c->stream));
       } else {
         std::vector<long long> word0(word);
         if (c->Kw > 0 && d.quad_lift.empty()) throw prismdg::ConfigError("device path needs the quad lifts");
@@ -540,7 +543,7 @@ void destroy_context(pdg_ctx* c) {
     cudaEventDestroy(pe.a);
     cudaEventDestroy(pe.b);
   }
-  void* ptrs[] = {c->u[0], c->u[1], c->res, c->rhs, c->stage, c->wgeo, c->wconn, c->Lt, c->QL, c->wadg,
+  void* ptrs[] = {c->u[0], c->u[1], c->res, c->rhs, c->stage, c->wgeo, c->wconn, c->Lt, c->QL, c->wadg, c->wadg_frag,
                   c->tgeo, c->tconn, c->DrT, c->DsT, c->Dt, c->prof, c->wface_dev, c->tDrT,
                   c->tDsT, c->tDtT, c->tLiftT, c->tface, c->nbr_nodes, c->Mtri, c->Xr, c->Xs,
                   c->M1D, c->w1d, c->Mtet, c->partials, c->scalar, c->badflag, c->ticket, c->dev_to_ref,

@@ -30,6 +30,7 @@ struct pdg_ctx {
   double* Lt = nullptr;
   double* QL = nullptr;
   double* wadg = nullptr; // WADG shared tables (mass_mode == wadg)
+  double* wadg_frag = nullptr; // fragment-major copy of the big WADG tables
   bool wedge_simt = false; // low-order CUDA-core wedge kernel (compact L / quad-lift layout)
   double* tgeo = nullptr;
   int* tconn = nullptr;

@@ -98,6 +98,7 @@ struct StageParams {
   const double* __restrict__ Lt;
   const double* __restrict__ QL;
   const double* __restrict__ wadg; // WADG shared tables (null unless the mass mode is wadg)
+  const double* __restrict__ wadg_frag; // the same, fragment-major (global-memory table variant)
   // tets
   const double* __restrict__ tgeo;
   const int* __restrict__ tconn;
@@ -146,6 +147,8 @@ int wedge_simt_max_degree();
 cudaError_t launch_wedge_simt_stage(int N, const StageParams& p, cudaStream_t s); // low-order CUDA-core wedge kernel
 cudaError_t launch_tet_dmma_stage(int N, const StageParams& p, cudaStream_t s); // batched DMMA tet kernel (N <= 5)
 cudaError_t launch_wedge_wadg_stage(int N, const StageParams& p, cudaStream_t s); // WADG (DMMA) kernel
+size_t wadg_frag_size(int N);
+cudaError_t launch_wadg_frag_fill(int N, const double* wadg, double* out, cudaStream_t s);
 /// Mtilde-norm wedge energy partials, one per block of wadg_energy_elems_per_block() wedges
 cudaError_t launch_wadg_energy(int N, const EnergyParams& p, int* nblocks_out, cudaStream_t s);
 int wedge_elems_per_block(int N);

@@ -47,7 +47,7 @@ __host__ __device__ constexpr int cf_stride(int x) {
 
 constexpr int kComboCapW = 2048; // ints of neighbour node maps kept in shared memory
 
-template <int N, int NST_>
+template <int N, int NST_, bool TG = false>
 struct WCfg {
   static constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npw_of(N), FW = fw_of(N), WG = wg_of(N);
   static constexpr int IT = it_of(N), KS = ks_of(N), KT = kt_of(N);
@@ -60,8 +60,10 @@ struct WCfg {
   static constexpr int PQT = IT * KQ * 32;       // Pw (A layout) / Vq (B layout)
   static constexpr int RT = IT * 3 * KT * 32;    // R0 or R1, all three faces
   static constexpr int DTT = JT * KT * 32;
-  static constexpr int TABLES =
-      r2(6 * KDT + 2 * PQT + 2 * RT + DTT + 2 * NQ + 2 * NC + ceil_div(FW, 2) + kComboCapW / 2);
+  static constexpr int BIGTAB = 6 * KDT + 2 * PQT + 2 * RT; // K-folded, Pw, Vq, R tables
+  // TG: the big tables stay in global memory (fragment-major, L1-resident) and
+  // shared memory only holds the small ones, leaving room for more teams
+  static constexpr int TABLES = r2((TG ? 0 : BIGTAB) + DTT + 2 * NQ + 2 * NC + ceil_div(FW, 2) + kComboCapW / 2);
   // per-stage buffers: state, residual, record + connectivity
   static constexpr int USTR = r4(4 * NP) + 2;
   static constexpr int STAGE = r2(2 * USTR + WG + kWC / 2);
@@ -95,6 +97,9 @@ inline int ticket_batch(int N) {
   return N <= 3 ? 8 : 2; // measured sweep, round 1 (profiles/round1_ticket_batch.txt)
 }
 
+/// big WADG tables in L1-cached global memory instead of shared memory
+inline bool wadg_tables_global_default(int N) { return N >= 7; } // measured: profiles/round1_wadg_tables.txt
+
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(d[0]), "+d"(d[1])
@@ -103,6 +108,42 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 
 __device__ __forceinline__ void team_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+/// fragment-major big tables [kd_m][Pw][Vq][R_m,e] from the flat WadgTables layout
+template <int N>
+__device__ void fill_wadg_tables(double* dst, const double* W, int tid, int nthr) {
+  using C = WCfg<N, 1>;
+  constexpr int NT = C::NT, NQ = C::NQ, NC = C::NC, IT = C::IT, KS = C::KS, KT = C::KT, KQ = C::KQ;
+  double* sKD = dst;
+  double* sPw = sKD + 6 * C::KDT;
+  double* sVq = sPw + C::PQT;
+  double* sR = sVq + C::PQT;
+  for (int q = tid; q < 6 * C::KDT; q += nthr) {
+    const int lane = q & 31, rest = q >> 5;
+    const int s = rest % KS, t = (rest / KS) % IT, m = rest / (KS * IT);
+    const int i = 8 * t + (lane >> 2), k = 4 * s + (lane & 3);
+    sKD[q] = (i < NT && k < NT) ? W[(m * NT + i) * NT + k] : 0.0;
+  }
+  for (int q = tid; q < C::PQT; q += nthr) {
+    const int lane = q & 31, rest = q >> 5;
+    const int s = rest % KQ, t = rest / KQ;
+    const int r = 8 * t + (lane >> 2), k = 4 * s + (lane & 3);
+    const bool in = r < NT && k < NC;
+    sPw[q] = in ? W[wadg_off_pw(N) + r * NC + k] : 0.0;
+    sVq[q] = in ? W[wadg_off_vq(N) + k * NT + r] : 0.0;
+  }
+  for (int q = tid; q < 2 * C::RT; q += nthr) {
+    const int lane = q & 31, rest = q >> 5;
+    const int s = rest % KT, e = (rest / KT) % 3, t = (rest / (3 * KT)) % IT, m = rest / (3 * KT * IT);
+    const int i = 8 * t + (lane >> 2), a = 4 * s + (lane & 3);
+    sR[q] = (i < NT && a < NQ) ? W[wadg_off_r(N) + ((m * 3 + e) * NT + i) * NQ + a] : 0.0;
+  }
+}
+
+template <int N>
+__global__ void wadg_frag_kernel(const double* __restrict__ W, double* __restrict__ out) {
+  fill_wadg_tables<N>(out, W, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 
 template <int N, int NST>
@@ -122,21 +163,18 @@ __device__ __forceinline__ void load_element(const StageParams& p, double* stg, 
   tma_load_1d_hint(G + C::WG, p.wconn + e * kWC, 4 * kWC, bar, stream);
 }
 
-template <int N, bool COMBO_SMEM, bool FUSED, int NST>
-__global__ void __launch_bounds__(WCfg<N, NST>::THREADS, 1) wedge_wadg_kernel(const StageParams p) {
-  using C = WCfg<N, NST>;
+template <int N, bool COMBO_SMEM, bool FUSED, int NST, bool TG>
+__global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kernel(const StageParams p) {
+  using C = WCfg<N, NST, TG>;
   constexpr int NQ = C::NQ, NT = C::NT, NP = C::NP, FW = C::FW, WG = C::WG, T = C::T;
   constexpr int IT = C::IT, KS = C::KS, KT = C::KT, KQ = C::KQ, NC = C::NC, JT = C::JT, CT = C::CT;
   constexpr int BST = C::BST;
   constexpr int QL_ = C::QF_LANE;
   extern __shared__ __align__(16) double smem[];
 
-  // ---- shared tables (fragment-major, zero padded) ---------------------------
-  double* sKD = smem;                 // [m][t][s][lane] = kd_m(8t+gid, 4s+tig)
-  double* sPw = sKD + 6 * C::KDT;     // [t][s][lane]    = Pw(8t+gid, 4s+tig)
-  double* sVq = sPw + C::PQT;         // [ct][s][lane]   = Vq(4s+tig, 8ct+gid)
-  double* sR = sVq + C::PQT;          // [m][t][e][s][lane] = R_m,e(8t+gid, 4s+tig)
-  double* sDt = sR + 2 * C::RT;       // [jt][s][lane]   = Dt(8jt+gid, 4s+tig)
+  // ---- tables (fragment-major, zero padded) -----------------------------------
+  double* sSmall = smem + (TG ? 0 : C::BIGTAB);
+  double* sDt = sSmall;               // [jt][s][lane]   = Dt(8jt+gid, 4s+tig)
   double* sProf = sDt + C::DTT;       // [2][NQ]
   double* sQr = sProf + 2 * NQ;       // [NC]
   double* sQs = sQr + NC;             // [NC]
@@ -145,27 +183,12 @@ __global__ void __launch_bounds__(WCfg<N, NST>::THREADS, 1) wedge_wadg_kernel(co
   for (int q = threadIdx.x; q < (int)(C::SMEM_BYTES / 8); q += C::THREADS) smem[q] = 0.0;
   __syncthreads();
   const double* W = p.wadg;
-  for (int q = threadIdx.x; q < 6 * C::KDT; q += C::THREADS) {
-    const int lane = q & 31, rest = q >> 5;
-    const int s = rest % KS, t = (rest / KS) % IT, m = rest / (KS * IT);
-    const int i = 8 * t + (lane >> 2), k = 4 * s + (lane & 3);
-    if (i < NT && k < NT) sKD[q] = W[(m * NT + i) * NT + k];
-  }
-  for (int q = threadIdx.x; q < C::PQT; q += C::THREADS) {
-    const int lane = q & 31, rest = q >> 5;
-    const int s = rest % KQ, t = rest / KQ;
-    const int r = 8 * t + (lane >> 2), k = 4 * s + (lane & 3);
-    if (r < NT && k < NC) {
-      sPw[q] = W[wadg_off_pw(N) + r * NC + k];
-      sVq[q] = W[wadg_off_vq(N) + k * NT + r];
-    }
-  }
-  for (int q = threadIdx.x; q < 2 * C::RT; q += C::THREADS) {
-    const int lane = q & 31, rest = q >> 5;
-    const int s = rest % KT, e = (rest / KT) % 3, t = (rest / (3 * KT)) % IT, m = rest / (3 * KT * IT);
-    const int i = 8 * t + (lane >> 2), a = 4 * s + (lane & 3);
-    if (i < NT && a < NQ) sR[q] = W[wadg_off_r(N) + ((m * 3 + e) * NT + i) * NQ + a];
-  }
+  if (!TG) fill_wadg_tables<N>(smem, W, threadIdx.x, C::THREADS);
+  const double* tKD = TG ? p.wadg_frag : smem; // [m][t][s][lane] = kd_m(8t+gid, 4s+tig)
+  const double* tPw = tKD + 6 * C::KDT;        // [t][s][lane]    = Pw(8t+gid, 4s+tig)
+  const double* tVq = tPw + C::PQT;            // [ct][s][lane]   = Vq(4s+tig, 8ct+gid)
+  const double* tR = tVq + C::PQT;             // [m][t][e][s][lane] = R_m,e(8t+gid, 4s+tig)
+  auto tab = [](const double* t, int idx) -> double { return TG ? __ldg(t + idx) : t[idx]; };
   for (int q = threadIdx.x; q < C::DTT; q += C::THREADS) {
     const int lane = q & 31, js = q >> 5, jt = js / KT, s = js - jt * KT;
     const int j = 8 * jt + (lane >> 2), l = 4 * s + (lane & 3);
@@ -332,9 +355,9 @@ __global__ void __launch_bounds__(WCfg<N, NST>::THREADS, 1) wedge_wadg_kernel(co
     for (int ct = 0; ct < IT; ++ct) lt[ct][0] = lt[ct][1] = 0.0;
 #pragma unroll
     for (int s2 = 0; s2 < KQ; ++s2) {
-      const double a = sPw[((t * KQ + s2) << 5) + lane] * sIJ[4 * s2 + tig];
+      const double a = tab(tPw, ((t * KQ + s2) << 5) + lane) * sIJ[4 * s2 + tig];
 #pragma unroll
-      for (int ct = 0; ct < IT; ++ct) dmma(lt[ct], a, sVq[((ct * KQ + s2) << 5) + lane]);
+      for (int ct = 0; ct < IT; ++ct) dmma(lt[ct], a, tab(tVq, ((ct * KQ + s2) << 5) + lane));
     }
 
     // ---- B: K-folded gradients gx, gy and divergence parts dvx, dvy ----------
@@ -354,7 +377,7 @@ __global__ void __launch_bounds__(WCfg<N, NST>::THREADS, 1) wedge_wadg_kernel(co
         double ax = 0.0, ay = 0.0;
 #pragma unroll
         for (int m = 0; m < 6; ++m) {
-          const double d = sKD[m * C::KDT + fo];
+          const double d = tab(tKD, m * C::KDT + fo);
           ax += cx[m] * d;
           ay += cy[m] * d;
         }
@@ -406,7 +429,7 @@ __global__ void __launch_bounds__(WCfg<N, NST>::THREADS, 1) wedge_wadg_kernel(co
 #pragma unroll
         for (int s2 = 0; s2 < KT; ++s2) {
           const int ro = (((t * 3 + f) * KT + s2) << 5) + lane;
-          const double qa = jf0 * sR[ro] + jf1 * sR[C::RT + ro];
+          const double qa = jf0 * tab(tR, ro) + jf1 * tab(tR, C::RT + ro);
 #pragma unroll
           for (int jt = 0; jt < JT; ++jt) {
             const int fo = (((f * JT + jt) * KT + s2) << 5) + lane;
@@ -510,11 +533,11 @@ __global__ void __launch_bounds__(WCfg<N, NST>::THREADS, 1) wedge_wadg_kernel(co
   }
 }
 
-template <int N, bool CS, bool FUSED, int NST>
+template <int N, bool CS, bool FUSED, int NST, bool TG>
 cudaError_t launch_wadg_NC(const StageParams& p, cudaStream_t s) {
-  using C = WCfg<N, NST>;
+  using C = WCfg<N, NST, TG>;
   static int grid_cap = 0;
-  auto kern = wedge_wadg_kernel<N, CS, FUSED, C::NSTAGE>;
+  auto kern = wedge_wadg_kernel<N, CS, FUSED, C::NSTAGE, TG>;
   if (grid_cap == 0) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
     if (err != cudaSuccess) return err;
@@ -536,6 +559,16 @@ cudaError_t launch_wadg_NC(const StageParams& p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+template <int N, bool TG>
+cudaError_t launch_wadg_NT(const StageParams& p, cudaStream_t s, bool fused, bool cs, int stages) {
+  if (stages == 1) {
+    if (fused) return cs ? launch_wadg_NC<N, true, true, 1, TG>(p, s) : launch_wadg_NC<N, false, true, 1, TG>(p, s);
+    return cs ? launch_wadg_NC<N, true, false, 1, TG>(p, s) : launch_wadg_NC<N, false, false, 1, TG>(p, s);
+  }
+  if (fused) return cs ? launch_wadg_NC<N, true, true, 2, TG>(p, s) : launch_wadg_NC<N, false, true, 2, TG>(p, s);
+  return cs ? launch_wadg_NC<N, true, false, 2, TG>(p, s) : launch_wadg_NC<N, false, false, 2, TG>(p, s);
+}
+
 template <int N>
 cudaError_t launch_wadg_N(const StageParams& p, cudaStream_t s) {
   constexpr int F = M_VOLUME | M_SURFACE | M_MEDIA | M_LSERK;
@@ -545,12 +578,12 @@ cudaError_t launch_wadg_N(const StageParams& p, cudaStream_t s) {
     const char* v = std::getenv("PDG_WEDGE_STAGES");
     return (v && v[0] == '1') ? 1 : 2;
   }();
-  if (stages == 1) {
-    if (fused) return cs ? launch_wadg_NC<N, true, true, 1>(p, s) : launch_wadg_NC<N, false, true, 1>(p, s);
-    return cs ? launch_wadg_NC<N, true, false, 1>(p, s) : launch_wadg_NC<N, false, false, 1>(p, s);
-  }
-  if (fused) return cs ? launch_wadg_NC<N, true, true, 2>(p, s) : launch_wadg_NC<N, false, true, 2>(p, s);
-  return cs ? launch_wadg_NC<N, true, false, 2>(p, s) : launch_wadg_NC<N, false, false, 2>(p, s);
+  static const int tables = [] { // 0 default, 1 shared, 2 global
+    const char* v = std::getenv("PDG_WADG_TABLES");
+    return v ? (v[0] == 's' ? 1 : 2) : 0;
+  }();
+  const bool tg = tables == 2 || (tables == 0 && wadg_tables_global_default(N));
+  return tg ? launch_wadg_NT<N, true>(p, s, fused, cs, stages) : launch_wadg_NT<N, false>(p, s, fused, cs, stages);
 }
 
 // ---------------------------------------------------------------------------
@@ -665,6 +698,24 @@ cudaError_t launch_wadg_energy_N(const EnergyParams& p, int* nb, cudaStream_t s)
 cudaError_t launch_wedge_wadg_stage(int N, const StageParams& p, cudaStream_t s) {
   switch (N) {
 #define PDG_CASE(n) case n: return launch_wadg_N<n>(p, s);
+    PDG_CASE(1) PDG_CASE(2) PDG_CASE(3) PDG_CASE(4) PDG_CASE(5) PDG_CASE(6) PDG_CASE(7)
+#undef PDG_CASE
+  }
+  return cudaErrorInvalidValue;
+}
+
+size_t wadg_frag_size(int N) {
+  switch (N) {
+#define PDG_CASE(n) case n: return (size_t)WCfg<n, 1>::BIGTAB;
+    PDG_CASE(1) PDG_CASE(2) PDG_CASE(3) PDG_CASE(4) PDG_CASE(5) PDG_CASE(6) PDG_CASE(7)
+#undef PDG_CASE
+  }
+  return 0;
+}
+
+cudaError_t launch_wadg_frag_fill(int N, const double* wadg, double* out, cudaStream_t s) {
+  switch (N) {
+#define PDG_CASE(n) case n: wadg_frag_kernel<n><<<64, 256, 0, s>>>(wadg, out); return cudaGetLastError();
     PDG_CASE(1) PDG_CASE(2) PDG_CASE(3) PDG_CASE(4) PDG_CASE(5) PDG_CASE(6) PDG_CASE(7)
 #undef PDG_CASE
   }
