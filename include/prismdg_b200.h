@@ -153,6 +153,11 @@ int pdg_get_rhs(pdg_ctx* ctx, double* rhs, int on_device);
 /* nsteps LSERK45 steps of TimeStepper::step (solver.cpp:536-557) on the
  * resident state; *t_inout += nsteps*dt.  Asynchronous on the context stream. */
 int pdg_step_lserk(pdg_ctx* ctx, double dt, int nsteps, double* t_inout);
+/* nsteps AB3 steps (TimeStepper::step with IntegratorKind::ab3, solver.cpp:559-581):
+ * the first two steps after pdg_set_state record f and take an LSERK45 step
+ * (bootstrap), then u += dt/12 (23 f_n - 16 f_{n-1} + 5 f_{n-2}).  The f
+ * history lives on the device and is reset by pdg_set_state. */
+int pdg_step_ab3(pdg_ctx* ctx, double dt, int nsteps, double* t_inout);
 /* compute_energy (solver.hpp:78): deterministic device reduction */
 int pdg_energy(pdg_ctx* ctx, double* energy);
 /* watchdog scan (solver.cpp:647-655): first element (reference id) with a
@@ -197,7 +202,7 @@ typedef struct {
   double energy_interval; /* 0: log every step */
   int watchdog_every;
   double blowup_factor;
-  int integrator;         /* 0 lserk4 */
+  int integrator;         /* 0 lserk4, 1 ab3 (dt = estimate * 0.25, solver.hpp:114) */
 } pdg_run_options;
 
 typedef struct {

@@ -453,6 +453,25 @@ void lserk_steps(const Discretization& d, double* u, std::size_t n, double dt, i
   }
 }
 
+void ab3_steps(const Discretization& d, double* u, std::size_t n, double dt, int nsteps, int threads) {
+  // solver.cpp:559-581; h[2] = f_{n-2}, h[1] = f_{n-1}
+  std::vector<std::vector<double>> h(3, std::vector<double>(n, 0.0));
+  std::vector<double> f(n);
+  int filled = 0;
+  for (int step = 0; step < nsteps; ++step) {
+    if (filled < 2) {
+      compute_rhs(d, u, h[2 - filled].data(), threads);
+      lserk_steps(d, u, n, dt, 1, threads, false);
+      ++filled;
+      continue;
+    }
+    compute_rhs(d, u, f.data(), threads);
+    for (std::size_t i = 0; i < n; ++i) u[i] += dt / 12.0 * (23.0 * f[i] - 16.0 * h[1][i] + 5.0 * h[2][i]);
+    std::swap(h[2], h[1]);
+    std::swap(h[1], f);
+  }
+}
+
 RunOut run_simulation(const Discretization& d, std::vector<double>& u, double& time, double final_time, double cfl,
                       double fixed_dt, double energy_interval, int threads) {
   // solver.cpp:591-666 (LSERK, watchdog every 50 steps, blow-up factor 10)

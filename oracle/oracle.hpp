@@ -55,6 +55,10 @@ double compute_energy(const Discretization& d, const double* u, int threads);
 void lserk_steps(const Discretization& d, double* u, std::size_t n, double dt, int nsteps, int threads,
                  bool parallel_update);
 
+/// nsteps of TimeStepper::step with IntegratorKind::ab3 from an empty history
+/// (solver.cpp:559-581): two LSERK45 bootstrap steps recording f, then AB3
+void ab3_steps(const Discretization& d, double* u, std::size_t n, double dt, int nsteps, int threads);
+
 struct RunOut {
   int steps = 0;
   double dt = 0, final_time = 0, initial_energy = 0, final_energy = 0, max_energy_increase = 0;

@@ -134,6 +134,7 @@ SIGNATURES = {
     "pdg_tet_surface": (C.c_int, [P]),
     "pdg_get_rhs": (C.c_int, [P, P, C.c_int]),
     "pdg_step_lserk": (C.c_int, [P, C.c_double, C.c_int, DP]),
+    "pdg_step_ab3": (C.c_int, [P, C.c_double, C.c_int, DP]),
     "pdg_energy": (C.c_int, [P, DP]),
     "pdg_check_finite": (C.c_int, [P, I64P]),
     "pdg_synchronize": (C.c_int, [P]),

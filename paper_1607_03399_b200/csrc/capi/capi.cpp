@@ -462,6 +462,16 @@ int pdg_step_lserk(pdg_ctx* ctx, double dt, int nsteps, double* t_inout) {
   });
 }
 
+int pdg_step_ab3(pdg_ctx* ctx, double dt, int nsteps, double* t_inout) {
+  return guarded([&] {
+    need(ctx, "context");
+    if (nsteps < 0) throw ConfigError("nsteps must be >= 0");
+    pdg::step_ab3(ctx, dt, nsteps);
+    if (t_inout)
+      for (int n = 0; n < nsteps; ++n) *t_inout += dt;
+  });
+}
+
 int pdg_energy(pdg_ctx* ctx, double* energy) {
   return guarded([&] {
     need(ctx, "context");
@@ -517,11 +527,13 @@ int pdg_run_simulation(pdg_ctx* ctx, double* u_inout, double* time_inout, const 
   return guarded([&] {
     need(ctx, "context");
     need(opts, "options");
-    if (opts->integrator != 0) throw ConfigError("device run driver supports lserk4 only");
+    if (opts->integrator != 0 && opts->integrator != 1) throw ConfigError("unknown integrator");
+    const bool ab3 = opts->integrator == 1;
     if (!(opts->final_time > *time_inout)) throw ConfigError("final time must exceed the state time");
     if (opts->watchdog_every < 1) throw ConfigError("watchdog_every must be >= 1");
     const double span = opts->final_time - *time_inout;
-    const double dt0 = opts->fixed_dt > 0.0 ? opts->fixed_dt : estimate_dt(*ctx->disc, opts->cfl);
+    // TimeStepper::dt_scale (solver.hpp:114): AB3 runs at a quarter of the LSERK step
+    const double dt0 = opts->fixed_dt > 0.0 ? opts->fixed_dt : estimate_dt(*ctx->disc, opts->cfl) * (ab3 ? 0.25 : 1.0);
     const int steps = std::max(1, (int)std::ceil(span / dt0 - 1e-12));
     const double dt = span / steps;
     pdg::set_state(ctx, u_inout, false);
@@ -544,7 +556,10 @@ int pdg_run_simulation(pdg_ctx* ctx, double* u_inout, double* time_inout, const 
     log_energy(t, res.initial_energy);
     double next_energy_t = t + opts->energy_interval;
     for (int n = 0; n < steps; ++n) {
-      pdg::step_lserk(ctx, dt, 1);
+      if (ab3)
+        pdg::step_ab3(ctx, dt, 1);
+      else
+        pdg::step_lserk(ctx, dt, 1);
       t += dt;
       if (opts->energy_interval <= 0.0) {
         log_energy(t, pdg::energy(ctx));

@@ -126,6 +126,15 @@ __global__ void tet_energy_kernel(const EnergyParams p, int block_offset) {
   if (n == 0) p.partials[block_offset + t] = red[0];
 }
 
+// AB3 update (TimeStepper::step, proj/src/solver.cpp:575-577):
+// u += dt/12 (23 f_n - 16 f_{n-1} + 5 f_{n-2}), elementwise over the whole state
+__global__ void ab3_update_kernel(long long n, double* __restrict__ u, const double* __restrict__ f0,
+                                  const double* __restrict__ f1, const double* __restrict__ f2, double c) {
+  for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+       idx += (long long)gridDim.x * blockDim.x)
+    u[idx] += c * (23.0 * f0[idx] - 16.0 * f1[idx] + 5.0 * f2[idx]);
+}
+
 __global__ void reduce_sum_kernel(const double* __restrict__ in, int n, double* __restrict__ out) {
   // single block, fixed order: strided partial sums then a tree
   __shared__ double red[1024];
@@ -233,6 +242,13 @@ cudaError_t launch_energy(int N, const EnergyParams& p, int* nblocks_out, cudaSt
     PDG_DISPATCH(N, (tet_energy_kernel<NN><<<(unsigned)p.Kt, npt_of(NN), 0, s>>>(p, wb)));
   }
   *nblocks_out = wb + (int)p.Kt;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ab3_update(long long n, double* u, const double* f0, const double* f1, const double* f2,
+                              double dt, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  ab3_update_kernel<<<148 * 8, 256, 0, s>>>(n, u, f0, f1, f2, dt / 12.0);
   return cudaGetLastError();
 }
 

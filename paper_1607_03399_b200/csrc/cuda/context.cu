@@ -547,6 +547,7 @@ void destroy_context(pdg_ctx* c) {
                   c->tgeo, c->tconn, c->DrT, c->DsT, c->Dt, c->prof, c->wface_dev, c->tDrT,
                   c->tDsT, c->tDtT, c->tLiftT, c->tface, c->nbr_nodes, c->Mtri, c->Xr, c->Xs,
                   c->M1D, c->w1d, c->Mtet, c->partials, c->scalar, c->badflag, c->ticket, c->dev_to_ref,
+                  c->fh[0], c->fh[1], c->fh[2],
                   c->ref_offset};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -563,6 +564,7 @@ void set_state(pdg_ctx* c, const double* u, bool on_device) {
     src = c->stage;
   }
   PDG_CK(launch_to_device_layout(c->N, c->Kw, c->Kt, c->dev_to_ref, c->ref_offset, src, c->u[c->cur], c->stream));
+  c->ab3_filled = 0; // a new state starts a new AB3 history
 }
 
 void get_state(pdg_ctx* c, double* u, bool on_device) {
@@ -638,6 +640,42 @@ void step_lserk(pdg_ctx* c, double dt, int nsteps) {
       if (s == 0) ++c->stage_launches_first; else ++c->stage_launches_later;
       c->cur = 1 - c->cur;
     }
+}
+
+// rhs of the current state (device layout) into dst: every kernel family in
+// rhs mode (volume + surface + media), as compute_rhs (solver.cpp:362-377)
+static void rhs_into(pdg_ctx* c, double* dst) {
+  StageParams p = base_params(c);
+  p.u_in = c->u[c->cur];
+  p.rhs_out = dst;
+  p.mode = M_VOLUME | M_SURFACE | M_MEDIA;
+  launch_checked(c, p, true);
+  launch_checked(c, p, false);
+}
+
+void step_ab3(pdg_ctx* c, double dt, int nsteps) {
+  PDG_CK(cudaSetDevice(c->device));
+  if (c->Kw_act != c->Kw || c->Kt_act != c->Kt)
+    throw prismdg::ConfigError("AB3 on a partitioned context is not supported");
+  const std::size_t nd = (std::size_t)c->total_dofs;
+  for (auto& h : c->fh)
+    if (!h) h = dalloc<double>(nd);
+  for (int n = 0; n < nsteps; ++n) {
+    if (c->ab3_filled < 2) {
+      // record f at the step start into h[2 - filled], then one LSERK step
+      rhs_into(c, c->fh[2 - c->ab3_filled]);
+      step_lserk(c, dt, 1);
+      ++c->ab3_filled;
+      continue;
+    }
+    rhs_into(c, c->fh[0]);
+    PDG_CK(launch_ab3_update((long long)nd, c->u[c->cur], c->fh[0], c->fh[1], c->fh[2], dt, c->stream));
+    // h[2] <- h[1], h[1] <- f_n, the old h[2] becomes the free slot
+    double* f2 = c->fh[2];
+    c->fh[2] = c->fh[1];
+    c->fh[1] = c->fh[0];
+    c->fh[0] = f2;
+  }
 }
 
 void stage_lserk(pdg_ctx* c, double dt, int s) {

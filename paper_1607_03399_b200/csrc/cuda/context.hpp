@@ -24,6 +24,10 @@ struct pdg_ctx {
   double* res = nullptr;
   double* rhs = nullptr;
   double* stage = nullptr; // reference-layout staging buffer (total_dofs)
+  // AB3 history (TimeStepper fhist_, solver.cpp:527-532): fh[0] free slot for
+  // f_n, fh[1] = f_{n-1}, fh[2] = f_{n-2}; allocated on first use
+  double* fh[3] = {nullptr, nullptr, nullptr};
+  int ab3_filled = 0;
 
   double* wgeo = nullptr;
   int* wconn = nullptr;
@@ -86,6 +90,8 @@ void compute_rhs(pdg_ctx* c, const double* u, double* rhs, bool on_device);
 void run_phase(pdg_ctx* c, bool wedge, bool volume);
 void get_rhs(pdg_ctx* c, double* rhs, bool on_device);
 void step_lserk(pdg_ctx* c, double dt, int nsteps);
+/// nsteps AB3 steps with the LSERK bootstrap of TimeStepper::step (solver.cpp:559-581)
+void step_ab3(pdg_ctx* c, double dt, int nsteps);
 double energy(pdg_ctx* c);
 long long check_finite(pdg_ctx* c);
 void synchronize(pdg_ctx* c);

@@ -155,6 +155,8 @@ int wedge_elems_per_block(int N);
 int tet_elems_per_block(int N);
 cudaError_t launch_energy(int N, const EnergyParams& p, int* nblocks_out, cudaStream_t s);
 cudaError_t launch_reduce_sum(const double* in, int n, double* out, cudaStream_t s);
+cudaError_t launch_ab3_update(long long n, double* u, const double* f0, const double* f1, const double* f2,
+                              double dt, cudaStream_t s);
 cudaError_t launch_to_device_layout(int N, long long Kw, long long Kt, const int* dev_to_ref,
                                     const long long* ref_offset, const double* src_ref,
                                     double* dst_dev, cudaStream_t s);

@@ -319,9 +319,11 @@ class DeviceContext:
         check(lib().pdg_get_rhs(self._h, p, dev))
         return out
 
-    def step(self, dt, nsteps=1, t=0.0):
+    def step(self, dt, nsteps=1, t=0.0, integrator="lserk4"):
+        """TimeStepper::step x nsteps on the resident state (lserk4 or ab3, solver.cpp:536-581)."""
         tt = C.c_double(t)
-        check(lib().pdg_step_lserk(self._h, dt, nsteps, C.byref(tt)))
+        fn = lib().pdg_step_ab3 if integrator == "ab3" else lib().pdg_step_lserk
+        check(fn(self._h, dt, nsteps, C.byref(tt)))
         return tt.value
 
     def energy(self):
@@ -409,6 +411,7 @@ class RunOptions:
     energy_interval: float = 0.0
     watchdog_every: int = 50
     blowup_factor: float = 10.0
+    integrator: str = "lserk4"  # IntegratorKind: "lserk4" | "ab3"
 
 
 @dataclass
@@ -425,7 +428,7 @@ class RunResult:
 def run_simulation(disc: Discretization, state: SolutionState, opts: RunOptions, max_log=100000) -> RunResult:
     """run_simulation (solver.hpp:148-149), state resident on the GPU for the run."""
     o = capi.RunOptions(opts.final_time, opts.cfl, opts.fixed_dt, opts.energy_interval,
-                        opts.watchdog_every, opts.blowup_factor, 0)
+                        opts.watchdog_every, opts.blowup_factor, 1 if opts.integrator == "ab3" else 0)
     r = capi.RunResult()
     log = np.zeros(2 * max_log)
     t = C.c_double(state.time)

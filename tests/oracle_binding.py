@@ -32,6 +32,7 @@ def lib():
         h.orc_phase.argtypes = [vp, C.c_int, dp, dp]
         h.orc_lserk.argtypes = [vp, dp, C.c_double, C.c_int, C.c_int, C.c_int]
         h.orc_energy.argtypes = [vp, dp, C.c_int, dp]
+        h.orc_ab3.argtypes = [vp, dp, C.c_double, C.c_int, C.c_int]
         h.orc_run.argtypes = [vp, dp, dp, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int, dp]
         h.orc_gll_newton.argtypes = [C.c_int, dp, dp]
         _lib = h
@@ -63,6 +64,12 @@ def phase(disc, which, u, rhs_inout):
 def lserk(disc, u, dt, nsteps, threads=4, parallel_update=True):
     u = np.array(u, dtype=np.float64, copy=True)
     _ok(lib().orc_lserk(disc.handle, _dp(u), dt, nsteps, threads, int(parallel_update)))
+    return u
+
+
+def ab3(disc, u, dt, nsteps, threads=4):
+    u = np.array(u, dtype=np.float64, copy=True)
+    _ok(lib().orc_ab3(disc.handle, _dp(u), dt, nsteps, threads))
     return u
 
 
