@@ -80,8 +80,8 @@ struct DCfg {
   static constexpr int TABLES = r2(2 * IT * KS * 32 + JT * KT * 32 + 2 * NQ + ceil_div(FW, 2) + kComboCap / 2);
   static constexpr int SMEM_BUDGET = 225 * 1024;
   // double-buffered stages unless even a single team would not fit
-  static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 2 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
-  static constexpr int PER_TEAM = 4 + NSTAGE * STAGE + WORK;
+  static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 6 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
+  static constexpr int PER_TEAM = 6 + NSTAGE * STAGE + WORK;
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
   // <= PDG_THREAD_CAP threads per CTA (512 keeps >= 128 registers per thread)
   static constexpr int TPB = cmax(1, cmin(cmin(15, PDG_THREAD_CAP / (32 * T)), TPB_SMEM)); // teams per CTA
@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
   const int bar_id = 1 + team;
   double* tbase = smem + C::TABLES + (size_t)team * C::PER_TEAM;
   uint64_t* bar = reinterpret_cast<uint64_t*>(tbase);
-  double* stg0 = tbase + 4; // 2 mbarriers + 2 schedule slots
+  double* stg0 = tbase + 6; // 2 mbarriers + 3 schedule slots + pad
   double* V = stg0 + NST * C::STAGE;
   double* Ftp = V + C::VS;      // tri-face fluxes: p part [2][NT]
   double* Ftu = Ftp + C::FTRI;  //                  u part
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
     long long en = 0;
     if (tt == 0) {
       en = grab();
-      slot[1] = en;
+      slot[1 + (n & 1)] = en; // parity slots: rewritten only after every thread read it
     }
     const double* U = stg0 + s * C::STAGE;
     const double* R = U + C::USTR;
@@ -495,8 +495,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
     }
     team_sync(bar_id, 32 * T); // stage s and the work buffers are free again
     if (NST == 1 && tt == 0 && en < p.Kw_active) load_element<N, NST>(p, stg0, en, res_src, bar);
-    e = slot[1];
-    team_sync(bar_id, 32 * T); // slot[1] is read by every thread before it is rewritten
+    e = slot[1 + (n & 1)];
   }
 }
 

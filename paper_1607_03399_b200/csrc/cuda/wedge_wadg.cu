@@ -75,8 +75,8 @@ struct WCfg {
   static constexpr int IJ = r2(4 * KQ);                      // 1/J at the cubature points
   static constexpr int WORK = BS + 2 * (FTRI + FQ) + IJ;
   static constexpr int SMEM_BUDGET = 225 * 1024;
-  static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 4 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
-  static constexpr int PER_TEAM = 4 + NSTAGE * STAGE + WORK;
+  static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 6 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
+  static constexpr int PER_TEAM = 6 + NSTAGE * STAGE + WORK;
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
   static constexpr int TPB = cmax(1, cmin(cmin(15, 512 / (32 * T)), TPB_SMEM)); // teams per CTA
   static constexpr int THREADS = 32 * T * TPB;
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
   const int bar_id = 1 + team;
   double* tbase = smem + C::TABLES + (size_t)team * C::PER_TEAM;
   uint64_t* bar = reinterpret_cast<uint64_t*>(tbase);
-  double* stg0 = tbase + 4;
+  double* stg0 = tbase + 6; // 2 mbarriers + 3 schedule slots + pad
   double* Bb = stg0 + NST * C::STAGE; // pre-lift buffer, column n = field*NQ + j, row = tri node
   double* Ftp = Bb + C::BS;           // [2][NT]
   double* Ftu = Ftp + C::FTRI;
@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
     long long en = 0;
     if (tt == 0) {
       en = grab();
-      slot[1] = en;
+      slot[1 + (n & 1)] = en; // parity slots: rewritten only after every thread read it
     }
     const double* U = stg0 + s * C::STAGE;
     const double* R = U + C::USTR;
@@ -528,8 +528,7 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
     }
     team_sync(bar_id, 32 * T); // stage s and the work buffers are free again
     if (NST == 1 && tt == 0 && en < p.Kw_active) load_element<N, NST>(p, stg0, en, res_src, bar);
-    e = slot[1];
-    team_sync(bar_id, 32 * T);
+    e = slot[1 + (n & 1)];
   }
 }
 
