@@ -45,6 +45,19 @@ def layered_workload(surface_n, sublayers):
     return pdg.layered_mesh(surface_n, [-1.0, -0.4, 0.2, 1.0], sublayers, [(1.0, 1.0), (1.0, 4.0), (1.0, 2.25)])
 
 
+def load_traffic(kind, degree):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of one stage
+    kernel from the committed ncu capture of the same workload (profiles/ncu_traffic.json,
+    made by scripts/make_traffic_json.py), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as fh:
+            tab = json.load(fh)
+        return float(tab[kind][str(degree)]["bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -221,7 +234,11 @@ def measure_degree(args, degree, ws, rank, local, peaks, with_e2e=True):
         "wedge_kernel_avg_ms": wedge_avg_ms, "wedge_stage_bytes": wbytes,
         "wedge_kernel_share": kt["wedge_ms"] / ms if ms > 0 else None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks[0], "unit": "GB/s",
-                     "frac": achieved / peaks[0], "traffic": None, "peak_source": peaks[1]},
+                     "frac": achieved / peaks[0], "peak_source": peaks[1],
+                     "traffic": load_traffic(("wadg" if mass == "wadg" else "exact") if mesh.num_tets() == 0
+                                             else "hybrid_wedge", degree),
+                     "traffic_unit": "bytes/launch (ncu, profiles/ncu_traffic.json)",
+                     "algorithmic_bytes": wbytes},
         "gpu_launches": int(kt["wedge_launches"] + kt["tet_launches"]),
         "tets": mesh.num_tets(),
         "clocks": clk.summary(),
@@ -231,7 +248,8 @@ def measure_degree(args, degree, ws, rank, local, peaks, with_e2e=True):
         res["tet_kernel_avg_ms"] = tet_avg_ms
         res["tet_kernel_share"] = kt["tet_ms"] / ms if ms > 0 else None
         res["tet_roofline"] = {"bound": "hbm", "achieved": t_ach, "peak": peaks[0], "unit": "GB/s",
-                               "frac": t_ach / peaks[0], "traffic": None, "peak_source": peaks[1]}
+                               "frac": t_ach / peaks[0], "peak_source": peaks[1],
+                               "traffic": load_traffic("tet", degree), "algorithmic_bytes": tbytes}
     if with_e2e:
         # e2e through the C ABI: pinned host state in, one step, state out, every step
         host = torch.empty(dofs, dtype=torch.float64, pin_memory=True)

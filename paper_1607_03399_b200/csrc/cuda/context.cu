@@ -390,12 +390,13 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags,
           return v && v[0] == 'd';
         }();
         c->wedge_simt = !force_dmma && N <= wedge_simt_max_degree();
-        if (c->wedge_simt) {
+        if (c->wedge_simt || wedge_dmma_compact_ops()) {
           // compact host layouts, no fragment padding: L [k][i], quad lifts [f][a][i]
-          c->Lt = dalloc<double>((std::size_t)c->Kw * nt * nt);
-          c->QL = dalloc<double>((std::size_t)c->Kw * 3 * nq * nt);
-          upload_permuted(c->Lt, d.tri_lift.data(), (std::size_t)nt * nt, word0);
-          upload_permuted(c->QL, d.quad_lift.data(), (std::size_t)3 * nq * nt, word0);
+          // (per-wedge stride padded to an even count for 16-byte TMA copies)
+          c->Lt = dalloc<double>((std::size_t)c->Kw * lcomp_of(N));
+          c->QL = dalloc<double>((std::size_t)c->Kw * qcomp_of(N));
+          upload_permuted(c->Lt, d.tri_lift.data(), (std::size_t)nt * nt, word0, lcomp_of(N));
+          upload_permuted(c->QL, d.quad_lift.data(), (std::size_t)3 * nq * nt, word0, qcomp_of(N));
         } else {
           c->Lt = dalloc<double>((std::size_t)c->Kw * lfrag_of(N));
           c->QL = dalloc<double>((std::size_t)c->Kw * qfrag_of(N));

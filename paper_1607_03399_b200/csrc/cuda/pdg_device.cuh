@@ -37,6 +37,10 @@ __host__ __device__ constexpr int kt_of(int N) { return ceil_div(nq_of(N), 4); }
 __host__ __device__ constexpr int lfrag_of(int N) { return it_of(N) * ks_of(N) * 32; }
 /// per-wedge quad lifts: [t][face][s][lane] = QL_face(8t+lane/4, 4s+lane%4)
 __host__ __device__ constexpr int qfrag_of(int N) { return it_of(N) * 3 * kt_of(N) * 32; }
+/// compact per-wedge operators (host layouts, padded to an even count for
+/// 16-byte TMA granularity): L [k][i], quad lifts [f][a][i]
+__host__ __device__ constexpr int lcomp_of(int N) { return even_up(nt_of(N) * nt_of(N)); }
+__host__ __device__ constexpr int qcomp_of(int N) { return even_up(3 * nq_of(N) * nt_of(N)); }
 
 // Weight-adjusted (WADG) shared tables, one flat array (built by the context
 // from prismdg::WadgTables, operators.hpp): row-major
@@ -152,6 +156,7 @@ cudaError_t launch_wadg_frag_fill(int N, const double* wadg, double* out, cudaSt
 /// Mtilde-norm wedge energy partials, one per block of wadg_energy_elems_per_block() wedges
 cudaError_t launch_wadg_energy(int N, const EnergyParams& p, int* nblocks_out, cudaStream_t s);
 int wedge_elems_per_block(int N);
+bool wedge_dmma_compact_ops(); // true: the DMMA wedge kernel reads compact L / quad lifts
 int tet_elems_per_block(int N);
 cudaError_t launch_energy(int N, const EnergyParams& p, int* nblocks_out, cudaStream_t s);
 cudaError_t launch_reduce_sum(const double* in, int n, double* out, cudaStream_t s);

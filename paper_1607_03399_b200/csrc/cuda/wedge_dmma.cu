@@ -55,8 +55,13 @@ constexpr int kComboCap = 4096; // ints of neighbour node maps kept in shared me
 #define PDG_WEDGE_STAGES 2
 #endif
 constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1 or 2)
+// compact L / quad lifts (no fragment padding in HBM; A fragments gathered
+// from the compact shared-memory copy) instead of fragment-major storage
+#ifndef PDG_COMPACT_OPS
+#define PDG_COMPACT_OPS 1
+#endif
 #ifndef PDG_THREAD_CAP
-#define PDG_THREAD_CAP 512
+#define PDG_THREAD_CAP 384
 #endif
 
 template <int N, int NST_>
@@ -66,7 +71,9 @@ struct DCfg {
   static constexpr int JT = ceil_div(NQ, 8), NPJ = 8 * JT;   // slice column tiles
   static constexpr int JTL = ceil_div(NQ + 2, 8);            // [P | Fu0 | Fu1] tiles
   static constexpr int T = IT;                               // warps per team
-  static constexpr int LF = lfrag_of(N), QF = qfrag_of(N);
+  // per-wedge operator block sizes in HBM / the stage buffer
+  static constexpr int LF = PDG_COMPACT_OPS ? lcomp_of(N) : lfrag_of(N);
+  static constexpr int QF = PDG_COMPACT_OPS ? qcomp_of(N) : qfrag_of(N);
   // per-stage buffers (doubles), 16-byte aligned
   static constexpr int USTR = r4(4 * NP) + 2;
   static constexpr int STAGE = r2(2 * USTR + LF + QF + WG + kWC / 2);
@@ -83,7 +90,8 @@ struct DCfg {
   static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 6 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
   static constexpr int PER_TEAM = 6 + NSTAGE * STAGE + WORK;
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
-  // <= PDG_THREAD_CAP threads per CTA (512 keeps >= 128 registers per thread)
+  // <= PDG_THREAD_CAP threads per CTA: 384 keeps >= 168 registers per thread
+  // (profiles/round1_compact_ops_ab.txt: compact operators + 384 beat 512)
   static constexpr int TPB = cmax(1, cmin(cmin(15, PDG_THREAD_CAP / (32 * T)), TPB_SMEM)); // teams per CTA
   static constexpr int THREADS = 32 * T * TPB;
   static constexpr size_t SMEM_BYTES = (size_t)8 * (TABLES + TPB * PER_TEAM);
@@ -369,7 +377,11 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
       for (int s2 = 0; s2 < KS; ++s2) {
         const int k = 4 * s2 + tig;
         const int fo = ((t * KS + s2) << 5) + lane;
+#if PDG_COMPACT_OPS
+        const double la = (i < NT && k < NT) ? Lf[k * NT + i] : 0.0;
+#else
         const double la = Lf[fo];
+#endif
         double cx = 0.0, cy = 0.0;
         if (vol) {
           const double dr = sDr[fo], ds = sDs[fo];
@@ -424,7 +436,12 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
         for (int f = 0; f < 3; ++f)
 #pragma unroll
           for (int s2 = 0; s2 < KT; ++s2) {
+#if PDG_COMPACT_OPS
+            const int qa_a = 4 * s2 + tig;
+            const double qa = (i < NT && qa_a < NQ) ? Qf[(f * NQ + qa_a) * NT + i] : 0.0;
+#else
             const double qa = Qf[(((t * 3 + f) * KT + s2) << 5) + lane];
+#endif
 #pragma unroll
             for (int jt = 0; jt < JT; ++jt) {
               const int fo = (((f * JT + jt) * KT + s2) << 5) + lane;
@@ -553,6 +570,8 @@ cudaError_t launch_wedge_stage(int N, const StageParams& p, cudaStream_t s) {
   }
   return cudaErrorInvalidValue;
 }
+
+bool wedge_dmma_compact_ops() { return PDG_COMPACT_OPS != 0; }
 
 int wedge_elems_per_block(int N) {
   switch (N) {

@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(SCfg<N>::THREADS, PDG_SIMT_MINB) wedge_simt_ke
     // per-thread operands from HBM: row i of L, rows i of the quad lifts, residual
     double Lr[NT], rres[4][NQ];
     if (active) {
-      const double* L = p.Lt + ge * NT * NT + i;
+      const double* L = p.Lt + ge * lcomp_of(N) + i;
 #pragma unroll
       for (int k = 0; k < NT; ++k) Lr[k] = __ldcs(L + k * NT);
 #pragma unroll
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(SCfg<N>::THREADS, PDG_SIMT_MINB) wedge_simt_ke
         }
       }
       if (surf) {
-        const double* QL = p.QL + ge * 3 * NQ * NT + i;
+        const double* QL = p.QL + ge * qcomp_of(N) + i;
         const double* nrm = G + w_nrm(N);
 #pragma unroll
         for (int f = 0; f < 3; ++f) {
