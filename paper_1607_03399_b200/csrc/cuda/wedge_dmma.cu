@@ -247,6 +247,37 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
   team_sync(bar_id, 32 * T);
   long long e = slot[0];
 
+  // neighbour traces of this thread's face-node tasks (prefetching the next
+  // element's during this element's products was measured slower: it exposes
+  // the next stage's TMA wait, profiles/round1_gather_prefetch_ab.txt)
+  double nb[QL_][4];
+  auto gather = [&](const int* Cg) {
+#pragma unroll
+    for (int q = 0; q < QL_; ++q) {
+      const int f = task_f[q];
+      if (f >= 0) {
+        const int nbr = Cg[2 * f];
+        if (nbr >= 0) {
+          const int mi = Cg[2 * f + 1] * p.max_nfp + task_loc[q];
+          const int node = COMBO_SMEM ? sCombo[mi] : __ldg(p.nbr_nodes + mi);
+          const double* src;
+          int fs;
+          if (nbr < p.Kw) {
+            src = p.u_in + (long long)nbr * 4 * NP + node;
+            fs = NP;
+          } else {
+            src = p.u_in + p.tet_base + (long long)(nbr - p.Kw) * 4 * npt_of(N) + node;
+            fs = npt_of(N);
+          }
+          nb[q][0] = __ldg(src);
+          nb[q][1] = __ldg(src + fs);
+          nb[q][2] = __ldg(src + 2 * fs);
+          nb[q][3] = __ldg(src + 3 * fs);
+        }
+      }
+    }
+  };
+
   for (int n = 0; e < p.Kw_active; ++n) {
     const int s = NST == 2 ? (n & 1) : 0;
     long long en = 0;
@@ -268,31 +299,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
 
     // ---- numerical fluxes on all face nodes -------------------------------------
     if (surf) {
-      double nb[QL_][4];
-#pragma unroll
-      for (int q = 0; q < QL_; ++q) {
-        const int f = task_f[q];
-        if (f >= 0) {
-          const int nbr = Cn[2 * f];
-          if (nbr >= 0) {
-            const int mi = Cn[2 * f + 1] * p.max_nfp + task_loc[q];
-            const int node = COMBO_SMEM ? sCombo[mi] : __ldg(p.nbr_nodes + mi);
-            const double* src;
-            int fs;
-            if (nbr < p.Kw) {
-              src = p.u_in + (long long)nbr * 4 * NP + node;
-              fs = NP;
-            } else {
-              src = p.u_in + p.tet_base + (long long)(nbr - p.Kw) * 4 * npt_of(N) + node;
-              fs = npt_of(N);
-            }
-            nb[q][0] = __ldg(src);
-            nb[q][1] = __ldg(src + fs);
-            nb[q][2] = __ldg(src + 2 * fs);
-            nb[q][3] = __ldg(src + 3 * fs);
-          }
-        }
-      }
+      gather(Cn);
 #pragma unroll
       for (int q = 0; q < QL_; ++q) {
         const int f = task_f[q];
