@@ -27,6 +27,8 @@
 // narrow window of the Morton-ordered element list).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "pdg_device.cuh"
 
 namespace pdg {
@@ -434,13 +436,20 @@ cudaError_t launch_simt_N(const StageParams& p, cudaStream_t s) {
 
 } // namespace
 
-int wedge_simt_max_degree() { return 3; }
+int wedge_simt_max_degree() {
+  static const int env = [] {
+    const char* v = std::getenv("PDG_SIMT_MAX_N");
+    return v ? std::atoi(v) : 0;
+  }();
+  return env > 0 ? (env < 4 ? env : 4) : 3;
+}
 
 cudaError_t launch_wedge_simt_stage(int N, const StageParams& p, cudaStream_t s) {
   switch (N) {
     case 1: return launch_simt_N<1>(p, s);
     case 2: return launch_simt_N<2>(p, s);
     case 3: return launch_simt_N<3>(p, s);
+    case 4: return launch_simt_N<4>(p, s);
   }
   return cudaErrorInvalidValue;
 }
