@@ -139,7 +139,8 @@ void launch_checked(pdg_ctx* c, const StageParams& p, bool wedge) {
     PDG_CK(cudaEventRecord(a, c->stream));
   }
   cudaError_t err = !wedge ? launch_tet_stage(c->N, p, c->stream)
-                    : c->wadg ? launch_wedge_wadg_stage(c->N, p, c->stream)
+                    : c->wadg ? (c->N <= wedge_wadg_simt_max_degree() ? launch_wedge_wadg_simt_stage(c->N, p, c->stream)
+                                                                     : launch_wedge_wadg_stage(c->N, p, c->stream))
                     : c->wedge_simt ? launch_wedge_simt_stage(c->N, p, c->stream)
                                     : launch_wedge_stage(c->N, p, c->stream);
   if (err != cudaSuccess) throw DeviceError(std::string("stage kernel launch failed: ") + cudaGetErrorString(err));

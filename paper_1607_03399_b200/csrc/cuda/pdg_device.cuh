@@ -149,6 +149,8 @@ cudaError_t launch_tet_stage(int N, const StageParams& p, cudaStream_t s);
 bool tet_dmma_supported(int N);
 int wedge_simt_max_degree();
 cudaError_t launch_wedge_simt_stage(int N, const StageParams& p, cudaStream_t s); // low-order CUDA-core wedge kernel
+int wedge_wadg_simt_max_degree();
+cudaError_t launch_wedge_wadg_simt_stage(int N, const StageParams& p, cudaStream_t s); // low-order WADG
 cudaError_t launch_tet_dmma_stage(int N, const StageParams& p, cudaStream_t s); // batched DMMA tet kernel (N <= 5)
 cudaError_t launch_wedge_wadg_stage(int N, const StageParams& p, cudaStream_t s); // WADG (DMMA) kernel
 size_t wadg_frag_size(int N);

@@ -71,7 +71,7 @@ __host__ __device__ constexpr int slot_stride(int x, int NT) {
 #define PDG_SIMT_MINB 1
 #endif
 
-template <int N>
+template <int N, bool WADG = false>
 struct SCfg {
   static constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npw_of(N), FW = fw_of(N), WG = wg_of(N);
   static constexpr int THREADS = PDG_SIMT_THREADS;
@@ -83,8 +83,12 @@ struct SCfg {
   static constexpr int FT = 4 * NT;                   // tri fluxes: [p|u][bottom|top][NT]
   static constexpr int FQ = 6 * NQ * NQ;              // quad fluxes: [p|u][face][a][j]
   static constexpr int SF = slot_stride(FT + FQ, NT);
-  static constexpr int SV = slot_stride(NQ * NT, NT); // V(j, i) at j*NT + i
-  static constexpr int TABLES = r2(r2(2 * NT * NT + NQ * NQ + 2 * NQ) + ceil_div(FW, 2) + 2048 / 2);
+  // exact: V(j, i) at j*NT + i; WADG: the pre-lift buffer B(field, j, i) + 1/J at the cubature
+  static constexpr int NC = wadg_nc(N);
+  static constexpr int SV = WADG ? slot_stride(4 * NQ * NT + NC, NT) : slot_stride(NQ * NT, NT);
+  // exact: Dr^T, Ds^T; WADG adds kd_m^T [m][k][i], Pw^T [q][i], Vq [q][k], R [m][f][a][i], qr, qs
+  static constexpr int WTAB = WADG ? 6 * NT * NT + 2 * NC * NT + 6 * NQ * NT + 2 * NC : 0;
+  static constexpr int TABLES = r2(r2(2 * NT * NT + NQ * NQ + 2 * NQ + WTAB) + ceil_div(FW, 2) + 2048 / 2);
   static constexpr size_t SMEM_BYTES = (size_t)8 * (TABLES + 2 * STAGE + E * (SF + SV) + 4);
   static constexpr int TASKS = ceil_div(E * FW, THREADS);
 };
@@ -101,9 +105,9 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 /// copy the state, record and connectivity of wedges [e0, e0+nel) into stage slots
-template <int N>
+template <int N, bool WADG>
 __device__ __forceinline__ void load_chunk(const StageParams& p, double* stg, long long e0, int nel) {
-  using C = SCfg<N>;
+  using C = SCfg<N, WADG>;
   constexpr int UV = 4 * C::NP / 2;     // 16-byte vectors per state block
   constexpr int GV = C::WG / 2;         // per record
   constexpr int CV = kWC / 4;           // per connectivity record (ints)
@@ -122,9 +126,9 @@ __device__ __forceinline__ void load_chunk(const StageParams& p, double* stg, lo
   }
 }
 
-template <int N>
-__global__ void __launch_bounds__(SCfg<N>::THREADS, PDG_SIMT_MINB) wedge_simt_kernel(const StageParams p) {
-  using C = SCfg<N>;
+template <int N, bool WADG>
+__global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB) wedge_simt_kernel(const StageParams p) {
+  using C = SCfg<N, WADG>;
   constexpr int NQ = C::NQ, NT = C::NT, NP = C::NP, FW = C::FW, WG = C::WG, E = C::E;
   constexpr int SU = C::SU, SG = C::SG, SF = C::SF, SV = C::SV;
   extern __shared__ __align__(16) double smem[];
@@ -132,7 +136,13 @@ __global__ void __launch_bounds__(SCfg<N>::THREADS, PDG_SIMT_MINB) wedge_simt_ke
   double* sDsT = sDrT + NT * NT;       // [k][i]
   double* sDt = sDsT + NT * NT;        // [j][l]
   double* sProf = sDt + NQ * NQ;       // [2][NQ]
-  int* sWface = reinterpret_cast<int*>(smem + r2(2 * NT * NT + NQ * NQ + 2 * NQ));
+  double* sKD = sProf + 2 * NQ;        // WADG: kd_m^T [m][k][i]
+  double* sPwT = sKD + 6 * NT * NT;    // WADG: Pw^T [q][i]
+  double* sVq = sPwT + C::NC * NT;     // WADG: Vq [q][k]
+  double* sR = sVq + C::NC * NT;       // WADG: R_m,f [m][f][a][i]
+  double* sQr = sR + 6 * NQ * NT;      // WADG: cubature points
+  double* sQs = sQr + C::NC;
+  int* sWface = reinterpret_cast<int*>(smem + r2(2 * NT * NT + NQ * NQ + 2 * NQ + C::WTAB));
   int* sCombo = sWface + 2 * ceil_div(FW, 2);
   double* stg = smem + C::TABLES;      // 2 stages
   double* sF = stg + 2 * C::STAGE;     // per wedge fluxes
@@ -145,6 +155,27 @@ __global__ void __launch_bounds__(SCfg<N>::THREADS, PDG_SIMT_MINB) wedge_simt_ke
   for (int q = threadIdx.x; q < NQ * NQ; q += C::THREADS) sDt[q] = p.Dt[q];
   for (int q = threadIdx.x; q < 2 * NQ; q += C::THREADS) sProf[q] = p.prof[q];
   for (int q = threadIdx.x; q < FW; q += C::THREADS) sWface[q] = p.wface_dev[q];
+  if (WADG) {
+    constexpr int NC = C::NC;
+    const double* W = p.wadg;
+    for (int q = threadIdx.x; q < 6 * NT * NT; q += C::THREADS) {
+      const int m = q / (NT * NT), r = q - m * NT * NT, k = r / NT, ii = r - k * NT;
+      sKD[q] = W[(m * NT + ii) * NT + k];
+    }
+    for (int q = threadIdx.x; q < NC * NT; q += C::THREADS) {
+      const int qq = q / NT, ii = q - qq * NT;
+      sPwT[q] = W[wadg_off_pw(N) + ii * NC + qq];
+      sVq[q] = W[wadg_off_vq(N) + q];
+    }
+    for (int q = threadIdx.x; q < 6 * NQ * NT; q += C::THREADS) {
+      const int mf = q / (NQ * NT), r = q - mf * NQ * NT, a = r / NT, ii = r - a * NT;
+      sR[q] = W[wadg_off_r(N) + (mf * NT + ii) * NQ + a];
+    }
+    for (int q = threadIdx.x; q < NC; q += C::THREADS) {
+      sQr[q] = W[wadg_off_q(N) + q];
+      sQs[q] = W[wadg_off_q(N) + NC + q];
+    }
+  }
   const bool combo_smem = p.nbr_nodes_len <= 2048;
   if (combo_smem)
     for (int q = threadIdx.x; q < p.nbr_nodes_len; q += C::THREADS) sCombo[q] = p.nbr_nodes[q];
@@ -166,7 +197,7 @@ __global__ void __launch_bounds__(SCfg<N>::THREADS, PDG_SIMT_MINB) wedge_simt_ke
   }
   __syncthreads();
   long long c = slot[0], cn = slot[1];
-  if (c < nchunk) load_chunk<N>(p, stg, c * E, nel_of(c));
+  if (c < nchunk) load_chunk<N, WADG>(p, stg, c * E, nel_of(c));
   cp_async_commit();
 
   const int el = threadIdx.x / NT, i = threadIdx.x - el * NT; // this thread's (wedge, node)
@@ -174,7 +205,7 @@ __global__ void __launch_bounds__(SCfg<N>::THREADS, PDG_SIMT_MINB) wedge_simt_ke
     double* cur = stg + (it & 1) * C::STAGE;
     // prefetch the next chunk into the other stage (it was released by the
     // trailing barrier of the previous iteration)
-    if (cn < nchunk) load_chunk<N>(p, stg + ((it + 1) & 1) * C::STAGE, cn * E, nel_of(cn));
+    if (cn < nchunk) load_chunk<N, WADG>(p, stg + ((it + 1) & 1) * C::STAGE, cn * E, nel_of(cn));
     cp_async_commit();
     cp_async_wait<1>();
     // next ticket; the slot alternates with the iteration parity so it is never
@@ -193,9 +224,11 @@ __global__ void __launch_bounds__(SCfg<N>::THREADS, PDG_SIMT_MINB) wedge_simt_ke
     // per-thread operands from HBM: row i of L, rows i of the quad lifts, residual
     double Lr[NT], rres[4][NQ];
     if (active) {
-      const double* L = p.Lt + ge * lcomp_of(N) + i;
+      if (!WADG) {
+        const double* L = p.Lt + ge * lcomp_of(N) + i;
 #pragma unroll
-      for (int k = 0; k < NT; ++k) Lr[k] = __ldcs(L + k * NT);
+        for (int k = 0; k < NT; ++k) Lr[k] = __ldcs(L + k * NT);
+      }
 #pragma unroll
       for (int f = 0; f < 4; ++f)
 #pragma unroll
@@ -270,8 +303,14 @@ __global__ void __launch_bounds__(SCfg<N>::THREADS, PDG_SIMT_MINB) wedge_simt_ke
         }
       }
     }
+    if (WADG)
+      for (int q = threadIdx.x; q < nel * C::NC; q += C::THREADS) {
+        const int e = q / C::NC, qq = q - e * C::NC;
+        const double* Ge = sG + e * SG;
+        sV[e * SV + 4 * NQ * NT + qq] = 1.0 / (Ge[w_jac(N)] + Ge[w_jac(N) + 1] * sQr[qq] + Ge[w_jac(N) + 2] * sQs[qq]);
+      }
     __syncthreads();
-
+    if constexpr (!WADG) {
     // ---- V column i, gradients, L products, quad lifts -------------------------------
     double rp[NQ], rux[NQ], ruy[NQ], ruz[NQ], lp[NQ];
     double lf0 = 0.0, lf1 = 0.0;
@@ -402,6 +441,134 @@ __global__ void __launch_bounds__(SCfg<N>::THREADS, PDG_SIMT_MINB) wedge_simt_ke
         }
       }
     }
+    } else {
+    // ---- WADG: Ltilde row i, pre-lift buffer B(field, j, i), then rhs = Ltilde B -------
+    constexpr int NC = C::NC;
+    double bp[NQ], bx[NQ], by[NQ], bz[NQ];
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) bp[j] = bx[j] = by[j] = bz[j] = 0.0;
+    if (active) {
+      const double* Fe = sF + el * SF;
+      const double* IJ = sV + el * SV + 4 * NQ * NT;
+      const double j0 = G[w_jac(N)], jr = G[w_jac(N) + 1], js = G[w_jac(N) + 2];
+      // Ltilde(i, :) = sum_q Pw(i, q) / J_q Vq(q, :)
+#pragma unroll
+      for (int k = 0; k < NT; ++k) Lr[k] = 0.0;
+      for (int q = 0; q < NC; ++q) {
+        const double a = sPwT[q * NT + i] * IJ[q];
+#pragma unroll
+        for (int k = 0; k < NT; ++k) Lr[k] += a * sVq[q * NT + k];
+      }
+      const double tzJ = G[W_TZJ];
+      if (vol) {
+        // K-folded horizontal derivatives: K (rx Dr + sx Ds) = sum_m c_m kd_m
+        const double rx = G[W_RX], ry = G[W_RY], sxm = G[W_SX], sym = G[W_SY];
+        const double cxm[6] = {rx * j0, rx * jr, rx * js, sxm * j0, sxm * jr, sxm * js};
+        const double cym[6] = {ry * j0, ry * jr, ry * js, sym * j0, sym * jr, sym * js};
+#pragma unroll
+        for (int k = 0; k < NT; ++k) {
+          double cx = 0.0, cy = 0.0;
+#pragma unroll
+          for (int m = 0; m < 6; ++m) {
+            const double d = sKD[(m * NT + k) * NT + i];
+            cx += cxm[m] * d;
+            cy += cym[m] * d;
+          }
+#pragma unroll
+          for (int j = 0; j < NQ; ++j) {
+            const double pk = U[j * NT + k];
+            bx[j] -= cx * pk;
+            by[j] -= cy * pk;
+            bp[j] -= cx * U[NP + j * NT + k] + cy * U[2 * NP + j * NT + k];
+          }
+        }
+        // vertical terms
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) {
+          const double sx_ = G[W_TXJ + j], sy_ = G[w_tyj(N) + j];
+          double d = 0.0, pdt = 0.0;
+#pragma unroll
+          for (int l = 0; l < NQ; ++l) {
+            const double dt = sDt[j * NQ + l];
+            d += U[NP + l * NT + i] * (sx_ * dt) + U[2 * NP + l * NT + i] * (sy_ * dt) + U[3 * NP + l * NT + i] * (tzJ * dt);
+            pdt += dt * U[l * NT + i];
+          }
+          bp[j] -= d;
+          bx[j] -= sx_ * pdt;
+          by[j] -= sy_ * pdt;
+          bz[j] -= tzJ * pdt;
+        }
+      }
+      if (surf) {
+        const double* nrm = G + w_nrm(N);
+        const double jfb = G[W_JFB], jft = G[W_JFT];
+        const double tpb = jfb * Fe[i], tpt = jft * Fe[NT + i], tub = jfb * Fe[2 * NT + i], tut = jft * Fe[3 * NT + i];
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) {
+          const double pb = sProf[j], pt = sProf[NQ + j];
+          bp[j] += tpb * pb + tpt * pt;
+          const double t0 = tub * pb, t1 = tut * pt;
+          bx[j] += nrm[0] * t0 + nrm[3] * t1;
+          by[j] += nrm[1] * t0 + nrm[4] * t1;
+          bz[j] += nrm[2] * t0 + nrm[5] * t1;
+        }
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+          const double jf0 = G[w_jac(N) + 3 + 2 * f], jf1 = G[w_jac(N) + 4 + 2 * f];
+          double qu[NQ];
+#pragma unroll
+          for (int j = 0; j < NQ; ++j) qu[j] = 0.0;
+#pragma unroll
+          for (int a = 0; a < NQ; ++a) {
+            const double q = jf0 * sR[(f * NQ + a) * NT + i] + jf1 * sR[((3 + f) * NQ + a) * NT + i];
+#pragma unroll
+            for (int j = 0; j < NQ; ++j) {
+              bp[j] += q * Fe[4 * NT + (f * NQ + a) * NQ + j];
+              qu[j] += q * Fe[4 * NT + 3 * NQ * NQ + (f * NQ + a) * NQ + j];
+            }
+          }
+          const double nx = nrm[3 * (f + 2)], ny = nrm[3 * (f + 2) + 1], nz = nrm[3 * (f + 2) + 2];
+#pragma unroll
+          for (int j = 0; j < NQ; ++j) {
+            bx[j] += nx * qu[j];
+            by[j] += ny * qu[j];
+            bz[j] += nz * qu[j];
+          }
+        }
+      }
+      double* Be = sV + el * SV;
+#pragma unroll
+      for (int j = 0; j < NQ; ++j) {
+        Be[j * NT + i] = bp[j];
+        Be[(NQ + j) * NT + i] = bx[j];
+        Be[(2 * NQ + j) * NT + i] = by[j];
+        Be[(3 * NQ + j) * NT + i] = bz[j];
+      }
+    }
+    __syncthreads(); // B complete
+    if (active) {
+      const double* Be = sV + el * SV;
+      const double kappa = G[W_KAPPA], irho = G[W_IRHO];
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int j = 0; j < NQ; ++j) {
+          double r = 0.0;
+#pragma unroll
+          for (int k = 0; k < NT; ++k) r += Lr[k] * Be[(f * NQ + j) * NT + k];
+          if (media) r *= f == 0 ? kappa : irho;
+          const int o = f * NP + j * NT + i;
+          const long long go = ge * 4 * NP + o;
+          if (lserk) {
+            const double rr = first ? p.dt * r : p.a * rres[f][j] + p.dt * r;
+            __stcs(p.res + go, rr);
+            __stcs(p.u_out + go, U[o] + p.b * rr);
+          } else {
+            __stcs(p.rhs_out + go, accum ? rres[f][j] + r : r);
+          }
+        }
+    }
+    }
     __syncthreads(); // the stage and the work buffers are free again
     c = cn;
     cn = slot[2 + (it & 1)];
@@ -409,11 +576,11 @@ __global__ void __launch_bounds__(SCfg<N>::THREADS, PDG_SIMT_MINB) wedge_simt_ke
   cp_async_wait<0>();
 }
 
-template <int N>
+template <int N, bool WADG>
 cudaError_t launch_simt_N(const StageParams& p, cudaStream_t s) {
-  using C = SCfg<N>;
+  using C = SCfg<N, WADG>;
   static int grid_cap = 0;
-  auto kern = wedge_simt_kernel<N>;
+  auto kern = wedge_simt_kernel<N, WADG>;
   if (grid_cap == 0) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
     if (err != cudaSuccess) return err;
@@ -446,10 +613,27 @@ int wedge_simt_max_degree() {
 
 cudaError_t launch_wedge_simt_stage(int N, const StageParams& p, cudaStream_t s) {
   switch (N) {
-    case 1: return launch_simt_N<1>(p, s);
-    case 2: return launch_simt_N<2>(p, s);
-    case 3: return launch_simt_N<3>(p, s);
-    case 4: return launch_simt_N<4>(p, s);
+    case 1: return launch_simt_N<1, false>(p, s);
+    case 2: return launch_simt_N<2, false>(p, s);
+    case 3: return launch_simt_N<3, false>(p, s);
+    case 4: return launch_simt_N<4, false>(p, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+int wedge_wadg_simt_max_degree() {
+  static const int env = [] {
+    const char* v = std::getenv("PDG_WADG_SIMT_MAX_N");
+    return v ? std::atoi(v) : -1;
+  }();
+  return env >= 0 ? (env < 3 ? env : 3) : 3;
+}
+
+cudaError_t launch_wedge_wadg_simt_stage(int N, const StageParams& p, cudaStream_t s) {
+  switch (N) {
+    case 1: return launch_simt_N<1, true>(p, s);
+    case 2: return launch_simt_N<2, true>(p, s);
+    case 3: return launch_simt_N<3, true>(p, s);
   }
   return cudaErrorInvalidValue;
 }
