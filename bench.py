@@ -321,8 +321,9 @@ def measure_degree_dist(args, degree, ws, rank, local, peaks):
     solver.close()
     return {"degree": degree, "value": value, "ms_per_step": ms / args.steps, "total_dofs": owned_dofs,
             "wedges": part.n_owned, "setup_s": round(setup_s, 1), "clocks": clk.summary(),
-            # per stage: one wedge stage kernel + one pack and one unpack per peer
-            "gpu_launches": args.steps * 5 * (1 + 2 * len(solver.peers)),
+            # per stage: interior + boundary wedge stage launches, one trace gather and
+            # one trace scatter per peer
+            "gpu_launches": args.steps * 5 * (2 + 2 * len(solver.peers)),
             "exchange_bytes_per_stage": solver.exchange_bytes}
 
 
@@ -366,7 +367,8 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (gaussian pulse on generated layered wedge mesh)",
                 "config": {"workload": "configs[4]: layered wedge slabs, 1e6 owned wedges per GPU stacked in z, "
-                                       "one ghost sublayer exchanged per LSERK stage (NCCL p2p)",
+                                       "face traces of the one-sublayer ghost layer exchanged per LSERK stage (NCCL p2p) "
+                                       "on a side stream, overlapped with the interior elements",
                            "degree": args.degree, "wedges_per_gpu": head["wedges"],
                            "parallelism": f"mesh partition x{ws}", "l2": "inputs larger than L2, no flush",
                            "exchange_bytes_per_stage_per_rank": head["exchange_bytes_per_stage"]},

@@ -193,6 +193,26 @@ int pdg_step_stage(pdg_ctx* ctx, double dt, int stage);
  * buffers: buf[k * 4 * max(Np_wedge, Np_tet) + ...] = state of dev_elems[k] */
 int pdg_pack_states(pdg_ctx* ctx, const int64_t* dev_elems, int64_t n, double* buf);
 int pdg_unpack_states(pdg_ctx* ctx, const int64_t* dev_elems, int64_t n, const double* buf);
+/* Owned elements are ordered interior (no ghost neighbour) first, then
+ * boundary.  counts[0..5] = owned wedges, owned tets, all wedges, all tets,
+ * interior wedges, interior tets. */
+int pdg_partition_counts(pdg_ctx* ctx, int64_t counts[6]);
+/* one LSERK stage over part 0 = all owned elements, 1 = interior only (needs
+ * no ghost data; does not complete the stage), 2 = boundary only (after the
+ * ghost refresh; completes the stage).  1 then 2 == 0, so the exchange can
+ * overlap the interior launch. */
+int pdg_step_stage_part(pdg_ctx* ctx, double dt, int stage, int part);
+/* face-trace exchange: state offsets (device layout) of 4 fields x face nodes
+ * of each (reference element, face) pair, written to out (host, capacity
+ * n * 4 * max face nodes); *count = entries written.  Both ranks enumerate the
+ * same pairs in the same order, so the lists align. */
+int pdg_trace_offsets(pdg_ctx* ctx, int64_t n, const int64_t* elems, const int* faces, int64_t* out,
+                      int64_t* count);
+/* buf[k] = state[idx[k]] / state[idx[k]] = buf[k] on the current state
+ * (device pointers).  stream: a cudaStream_t to issue on (e.g. an exchange
+ * stream overlapping the interior stage launch), or NULL for the context's. */
+int pdg_gather_values(pdg_ctx* ctx, const int64_t* idx, int64_t n, double* buf, void* stream);
+int pdg_scatter_values(pdg_ctx* ctx, const int64_t* idx, int64_t n, const double* buf, void* stream);
 
 /* ---------------------------------------------------------------- run driver */
 typedef struct {

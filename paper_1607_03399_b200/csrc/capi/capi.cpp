@@ -398,6 +398,49 @@ int pdg_active_counts(pdg_ctx* ctx, int64_t counts[4]) {
   });
 }
 
+int pdg_partition_counts(pdg_ctx* ctx, int64_t counts[6]) {
+  return guarded([&] {
+    need(ctx, "context");
+    counts[0] = ctx->Kw_act;
+    counts[1] = ctx->Kt_act;
+    counts[2] = ctx->Kw;
+    counts[3] = ctx->Kt;
+    counts[4] = ctx->Kw_int;
+    counts[5] = ctx->Kt_int;
+  });
+}
+
+int pdg_step_stage_part(pdg_ctx* ctx, double dt, int stage, int part) {
+  return guarded([&] {
+    need(ctx, "context");
+    pdg::stage_lserk(ctx, dt, stage, part);
+  });
+}
+
+int pdg_trace_offsets(pdg_ctx* ctx, int64_t n, const int64_t* elems, const int* faces, int64_t* out,
+                      int64_t* count) {
+  return guarded([&] {
+    need(ctx, "context");
+    static_assert(sizeof(int64_t) == sizeof(long long), "int64_t is long long");
+    *count = pdg::trace_offsets(ctx, n, reinterpret_cast<const long long*>(elems), faces,
+                                reinterpret_cast<long long*>(out));
+  });
+}
+
+int pdg_gather_values(pdg_ctx* ctx, const int64_t* idx, int64_t n, double* buf, void* stream) {
+  return guarded([&] {
+    need(ctx, "context");
+    pdg::gather_values(ctx, reinterpret_cast<const long long*>(idx), n, buf, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int pdg_scatter_values(pdg_ctx* ctx, const int64_t* idx, int64_t n, const double* buf, void* stream) {
+  return guarded([&] {
+    need(ctx, "context");
+    pdg::scatter_values(ctx, reinterpret_cast<const long long*>(idx), n, buf, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int pdg_step_stage(pdg_ctx* ctx, double dt, int stage) {
   return guarded([&] {
     need(ctx, "context");

@@ -245,6 +245,29 @@ cudaError_t launch_energy(int N, const EnergyParams& p, int* nblocks_out, cudaSt
   return cudaGetLastError();
 }
 
+// face-trace exchange of the multi-GPU path: buf[k] = u[idx[k]] / u[idx[k]] = buf[k]
+__global__ void gather_values_kernel(const long long* __restrict__ idx, long long n, const double* __restrict__ u,
+                                     double* __restrict__ buf) {
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+    buf[k] = u[idx[k]];
+}
+__global__ void scatter_values_kernel(const long long* __restrict__ idx, long long n, const double* __restrict__ buf,
+                                      double* __restrict__ u) {
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+    u[idx[k]] = buf[k];
+}
+
+cudaError_t launch_gather_values(const long long* idx, long long n, const double* u, double* buf, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  gather_values_kernel<<<(unsigned)((n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8), 256, 0, s>>>(idx, n, u, buf);
+  return cudaGetLastError();
+}
+cudaError_t launch_scatter_values(const long long* idx, long long n, const double* buf, double* u, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  scatter_values_kernel<<<(unsigned)((n + 255) / 256 < 148 * 8 ? (n + 255) / 256 : 148 * 8), 256, 0, s>>>(idx, n, buf, u);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_ab3_update(long long n, double* u, const double* f0, const double* f1, const double* f2,
                               double dt, cudaStream_t s) {
   if (n == 0) return cudaSuccess;

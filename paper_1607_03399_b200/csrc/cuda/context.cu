@@ -295,13 +295,28 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags,
     auto tord = locality_order(d.mesh, false, native);
     c->Kw_act = c->Kw;
     c->Kt_act = c->Kt;
-    if (owned) { // owned elements first, ghosts after (stable: keeps the locality order)
-      auto split = [&](std::vector<long long>& ord) {
-        std::stable_partition(ord.begin(), ord.end(), [&](long long r) { return owned[r] != 0; });
-        return (long long)std::count_if(ord.begin(), ord.end(), [&](long long r) { return owned[r] != 0; });
+    c->Kw_int = c->Kw;
+    c->Kt_int = c->Kt;
+    if (owned) {
+      // owned interior (no ghost neighbour) first, then owned boundary, then
+      // ghosts; stable, so each group keeps the locality order.  The interior
+      // stage launch can then run while the ghost traces are exchanged.
+      auto interior = [&](long long r) {
+        if (!owned[r]) return false;
+        for (int f = 0; f < d.mesh.num_faces((int)r); ++f) {
+          const int nb = d.conn.at((int)r, f).nbr;
+          if (nb >= 0 && !owned[nb]) return false;
+        }
+        return true;
       };
-      c->Kw_act = split(word);
-      c->Kt_act = split(tord);
+      auto split = [&](std::vector<long long>& ord, long long& n_act, long long& n_int) {
+        std::stable_partition(ord.begin(), ord.end(), [&](long long r) { return owned[r] != 0; });
+        n_act = (long long)std::count_if(ord.begin(), ord.end(), [&](long long r) { return owned[r] != 0; });
+        std::stable_partition(ord.begin(), ord.begin() + n_act, interior);
+        n_int = (long long)std::count_if(ord.begin(), ord.begin() + n_act, interior);
+      };
+      split(word, c->Kw_act, c->Kw_int);
+      split(tord, c->Kt_act, c->Kt_int);
     }
     c->dev_to_ref_host.resize(c->Kw + c->Kt);
     std::copy(word.begin(), word.end(), c->dev_to_ref_host.begin());
@@ -680,10 +695,18 @@ void step_ab3(pdg_ctx* c, double dt, int nsteps) {
   }
 }
 
-void stage_lserk(pdg_ctx* c, double dt, int s) {
+void stage_lserk(pdg_ctx* c, double dt, int s, int part) {
   PDG_CK(cudaSetDevice(c->device));
   if (s < 0 || s > 4) throw prismdg::ConfigError("LSERK stage index must be in [0,5)");
+  if (part < 0 || part > 2) throw prismdg::ConfigError("stage part must be 0 (all), 1 (interior) or 2 (boundary)");
   StageParams p = base_params(c);
+  if (part == 1) {
+    p.Kw_active = c->Kw_int;
+    p.Kt_active = c->Kt_int;
+  } else if (part == 2) {
+    p.Kw_begin = c->Kw_int;
+    p.Kt_begin = c->Kt_int;
+  }
   p.res = c->res;
   p.dt = dt;
   p.u_in = c->u[c->cur];
@@ -693,8 +716,40 @@ void stage_lserk(pdg_ctx* c, double dt, int s) {
   p.mode = M_VOLUME | M_SURFACE | M_MEDIA | M_LSERK | (s == 0 ? M_FIRST : 0);
   launch_checked(c, p, true);
   launch_checked(c, p, false);
+  if (part == 1) return; // the boundary part completes the stage
   if (s == 0) ++c->stage_launches_first; else ++c->stage_launches_later;
   c->cur = 1 - c->cur;
+}
+
+long long trace_offsets(pdg_ctx* c, long long n, const long long* elems, const int* faces, long long* out) {
+  const prismdg::Discretization& d = *c->disc;
+  std::vector<long long> ref_to_dev(c->dev_to_ref_host.size());
+  for (std::size_t q = 0; q < c->dev_to_ref_host.size(); ++q) ref_to_dev[c->dev_to_ref_host[q]] = (long long)q;
+  long long m = 0;
+  for (long long k = 0; k < n; ++k) {
+    const long long r = elems[k];
+    const int f = faces[k];
+    if (r < 0 || r >= (long long)ref_to_dev.size()) throw prismdg::ConfigError("trace element out of range");
+    const bool wedge = d.mesh.kind((int)r) == prismdg::ElemKind::wedge;
+    if (f < 0 || f >= d.mesh.num_faces((int)r)) throw prismdg::ConfigError("trace face out of range");
+    const long long dev = ref_to_dev[r];
+    const long long base = wedge ? dev * 4 * c->npw : c->tet_base + (dev - c->Kw) * 4 * c->npt;
+    const int np = wedge ? c->npw : c->npt;
+    const auto& nodes = d.my_nodes((int)r, f);
+    for (int fld = 0; fld < 4; ++fld)
+      for (int nref : nodes) out[m++] = base + (long long)fld * np + dev_node_of(d, wedge, nref);
+  }
+  return m;
+}
+
+void gather_values(pdg_ctx* c, const long long* idx, long long n, double* buf, cudaStream_t s) {
+  PDG_CK(cudaSetDevice(c->device));
+  PDG_CK(launch_gather_values(idx, n, c->u[c->cur], buf, s ? s : c->stream));
+}
+
+void scatter_values(pdg_ctx* c, const long long* idx, long long n, const double* buf, cudaStream_t s) {
+  PDG_CK(cudaSetDevice(c->device));
+  PDG_CK(launch_scatter_values(idx, n, buf, c->u[c->cur], s ? s : c->stream));
 }
 
 void pack_states(pdg_ctx* c, const long long* dev_elems, long long n, double* buf) {

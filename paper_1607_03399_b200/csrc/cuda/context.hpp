@@ -17,6 +17,7 @@ struct pdg_ctx {
   int N = 0, nq = 0, nt = 0, npw = 0, npt = 0, fw = 0;
   long long Kw = 0, Kt = 0, total_dofs = 0, tet_base = 0;
   long long Kw_act = 0, Kt_act = 0; // owned (computed) elements; ghosts follow them
+  long long Kw_int = 0, Kt_int = 0; // owned elements without ghost neighbours (they come first)
   prismdg::MassMode mass_mode = prismdg::MassMode::exact;
 
   double* u[2] = {nullptr, nullptr};
@@ -80,7 +81,15 @@ namespace pdg {
 /// ghosts are ordered after the owned elements of their kind.
 pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags,
                         const unsigned char* owned = nullptr);
-void stage_lserk(pdg_ctx* c, double dt, int stage);
+/// one LSERK stage over the owned elements (part 0), only the interior ones
+/// (part 1: no ghost data needed, state not flipped) or only the boundary ones
+/// (part 2: after the ghost refresh; flips the state)
+void stage_lserk(pdg_ctx* c, double dt, int stage, int part = 0);
+/// device-layout state offsets of the face traces (4 fields x face nodes) of
+/// (reference element, face) pairs; returns the number written
+long long trace_offsets(pdg_ctx* c, long long n, const long long* elems, const int* faces, long long* out);
+void gather_values(pdg_ctx* c, const long long* idx, long long n, double* buf, cudaStream_t s = nullptr);
+void scatter_values(pdg_ctx* c, const long long* idx, long long n, const double* buf, cudaStream_t s = nullptr);
 void pack_states(pdg_ctx* c, const long long* dev_elems, long long n, double* buf);
 void unpack_states(pdg_ctx* c, const long long* dev_elems, long long n, const double* buf);
 void destroy_context(pdg_ctx* c);

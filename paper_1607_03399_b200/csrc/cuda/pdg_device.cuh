@@ -88,7 +88,8 @@ enum : int {
 
 struct StageParams {
   long long Kw, Kt;               // all device elements (addressing)
-  long long Kw_active, Kt_active; // elements computed: owned ones come first, ghosts after
+  long long Kw_active, Kt_active; // end of the computed range: owned elements come first, ghosts after
+  long long Kw_begin, Kt_begin;   // start of the computed range (interior / boundary split launches)
   long long tet_base; // dof offset of the first tet block
   const double* __restrict__ u_in;
   double* __restrict__ u_out;
@@ -162,6 +163,8 @@ bool wedge_dmma_compact_ops(); // true: the DMMA wedge kernel reads compact L / 
 int tet_elems_per_block(int N);
 cudaError_t launch_energy(int N, const EnergyParams& p, int* nblocks_out, cudaStream_t s);
 cudaError_t launch_reduce_sum(const double* in, int n, double* out, cudaStream_t s);
+cudaError_t launch_gather_values(const long long* idx, long long n, const double* u, double* buf, cudaStream_t s);
+cudaError_t launch_scatter_values(const long long* idx, long long n, const double* buf, double* u, cudaStream_t s);
 cudaError_t launch_ab3_update(long long n, double* u, const double* f0, const double* f1, const double* f2,
                               double dt, cudaStream_t s);
 cudaError_t launch_to_device_layout(int N, long long Kw, long long Kt, const int* dev_to_ref,

@@ -149,17 +149,17 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
   const bool lserk = mode & M_LSERK, media = mode & M_MEDIA;
   const bool first = mode & M_FIRST, accum = mode & M_ACCUM;
   const double* res_src = lserk ? (first ? nullptr : p.res) : (accum ? p.rhs_out : nullptr);
-  const long long nbatch = (p.Kt_active + kTB - 1) / kTB;
+  const long long nbatch = (p.Kt_active - p.Kt_begin + kTB - 1) / kTB;
   volatile long long* slot = reinterpret_cast<volatile long long*>(bar + 2);
   auto grab = [&]() -> long long { return (long long)(atomicAdd(p.ticket, 1ULL) - p.ticket_base); };
   auto nel_of = [&](long long b) -> int {
-    const long long r = p.Kt_active - b * kTB;
+    const long long r = p.Kt_active - p.Kt_begin - b * kTB;
     return (int)(r < kTB ? r : kTB);
   };
   if (tt == 0) {
     const long long b0 = grab();
     slot[0] = b0;
-    if (b0 < nbatch) load_batch<N, NST>(p, stg0, b0 * kTB, nel_of(b0), bar);
+    if (b0 < nbatch) load_batch<N, NST>(p, stg0, p.Kt_begin + b0 * kTB, nel_of(b0), bar);
   }
   team_sync(bar_id, 32 * T);
   long long b = slot[0];
@@ -177,10 +177,10 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
     const int* Cn = reinterpret_cast<const int*>(G + kTB * kTG);
     if (NST == 2 && tt == 0 && bn < nbatch) {
       fence_proxy_async_smem();
-      load_batch<N, NST>(p, stg0 + (s ^ 1) * C::STAGE, bn * kTB, nel_of(bn), bar + (s ^ 1));
+      load_batch<N, NST>(p, stg0 + (s ^ 1) * C::STAGE, p.Kt_begin + bn * kTB, nel_of(bn), bar + (s ^ 1));
     }
     mbar_wait(bar + s, NST == 2 ? ((it >> 1) & 1) : (it & 1));
-    const long long t0 = b * kTB;
+    const long long t0 = p.Kt_begin + b * kTB;
     const int nel = nel_of(b);
     const int n = 8 * w + gid;
     // residual (or accumulated rhs) of this thread's 2 tets x 4 fields, loaded
@@ -345,7 +345,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
       }
     }
     team_sync(bar_id, 32 * T); // stage s and the work buffers are free again
-    if (NST == 1 && tt == 0 && bn < nbatch) load_batch<N, NST>(p, stg0, bn * kTB, nel_of(bn), bar);
+    if (NST == 1 && tt == 0 && bn < nbatch) load_batch<N, NST>(p, stg0, p.Kt_begin + bn * kTB, nel_of(bn), bar);
     b = slot[1];
     team_sync(bar_id, 32 * T);
   }
@@ -366,8 +366,8 @@ cudaError_t launch_tet_dmma_N(const StageParams& p, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM_BYTES);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
-  if (p.Kt_active == 0) return cudaSuccess;
-  const long long nbatch = (p.Kt_active + kTB - 1) / kTB;
+  if (p.Kt_active - p.Kt_begin <= 0) return cudaSuccess;
+  const long long nbatch = (p.Kt_active - p.Kt_begin + kTB - 1) / kTB;
   const long long need = (nbatch + C::TPB - 1) / C::TPB;
   const int grid = (int)(need < grid_cap ? need : grid_cap);
   StageParams q = p;

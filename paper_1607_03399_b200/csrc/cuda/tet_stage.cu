@@ -38,7 +38,7 @@ tet_stage_kernel(const StageParams p) {
   double* sG = sF + E * C::FSTR;
   int* sC = reinterpret_cast<int*>(sG + E * kTG);
 
-  const long long t0 = (long long)blockIdx.x * E;
+  const long long t0 = p.Kt_begin + (long long)blockIdx.x * E;
   const int nel = (int)((p.Kt_active - t0) < E ? (p.Kt_active - t0) : E);
   const int mode = p.mode;
   const double* ubase = p.u_in + p.tet_base;
@@ -180,8 +180,8 @@ cudaError_t launch_tet_N(const StageParams& p, cudaStream_t s) {
     if (err != cudaSuccess) return err;
     configured = true;
   }
-  if (p.Kt_active == 0) return cudaSuccess;
-  const long long blocks = (p.Kt_active + C::E - 1) / C::E;
+  if (p.Kt_active - p.Kt_begin <= 0) return cudaSuccess;
+  const long long blocks = (p.Kt_active - p.Kt_begin + C::E - 1) / C::E;
   tet_stage_kernel<N><<<(unsigned)blocks, C::THREADS, C::SMEM_BYTES, s>>>(p);
   return cudaGetLastError();
 }

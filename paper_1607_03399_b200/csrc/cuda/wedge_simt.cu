@@ -186,9 +186,9 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB) wedge_s
   const bool lserk = mode & M_LSERK, media = mode & M_MEDIA;
   const bool first = mode & M_FIRST, accum = mode & M_ACCUM;
   const double* res_src = lserk ? (first ? nullptr : p.res) : (accum ? p.rhs_out : nullptr);
-  const long long nchunk = (p.Kw_active + E - 1) / E;
+  const long long nchunk = (p.Kw_active - p.Kw_begin + E - 1) / E;
   auto nel_of = [&](long long c) -> int {
-    const long long r = p.Kw_active - c * E;
+    const long long r = p.Kw_active - p.Kw_begin - c * E;
     return (int)(r < E ? r : E);
   };
   if (threadIdx.x == 0) {
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB) wedge_s
   }
   __syncthreads();
   long long c = slot[0], cn = slot[1];
-  if (c < nchunk) load_chunk<N, WADG>(p, stg, c * E, nel_of(c));
+  if (c < nchunk) load_chunk<N, WADG>(p, stg, p.Kw_begin + c * E, nel_of(c));
   cp_async_commit();
 
   const int el = threadIdx.x / NT, i = threadIdx.x - el * NT; // this thread's (wedge, node)
@@ -205,14 +205,14 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB) wedge_s
     double* cur = stg + (it & 1) * C::STAGE;
     // prefetch the next chunk into the other stage (it was released by the
     // trailing barrier of the previous iteration)
-    if (cn < nchunk) load_chunk<N, WADG>(p, stg + ((it + 1) & 1) * C::STAGE, cn * E, nel_of(cn));
+    if (cn < nchunk) load_chunk<N, WADG>(p, stg + ((it + 1) & 1) * C::STAGE, p.Kw_begin + cn * E, nel_of(cn));
     cp_async_commit();
     cp_async_wait<1>();
     // next ticket; the slot alternates with the iteration parity so it is never
     // rewritten before every thread has read it
     if (threadIdx.x == 0) slot[2 + (it & 1)] = (long long)(atomicAdd(p.ticket, 1ULL) - p.ticket_base);
     __syncthreads();
-    const long long e0 = c * E;
+    const long long e0 = p.Kw_begin + c * E;
     const int nel = nel_of(c);
     const double* sU = cur;
     const double* sG = cur + E * SU;
@@ -590,8 +590,8 @@ cudaError_t launch_simt_N(const StageParams& p, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM_BYTES);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
-  if (p.Kw_active == 0) return cudaSuccess;
-  const long long nchunk = (p.Kw_active + C::E - 1) / C::E;
+  if (p.Kw_active - p.Kw_begin <= 0) return cudaSuccess;
+  const long long nchunk = (p.Kw_active - p.Kw_begin + C::E - 1) / C::E;
   const int grid = (int)(nchunk < grid_cap ? nchunk : grid_cap);
   StageParams q = p;
   q.ticket_base = *p.ticket_host_next;

@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
   long long bnext = 0, bend = 0;
   auto grab = [&]() -> long long {
     if (bnext >= bend) {
-      bnext = (long long)(atomicAdd(p.ticket, (unsigned long long)B) - p.ticket_base);
+      bnext = p.Kw_begin + (long long)(atomicAdd(p.ticket, (unsigned long long)B) - p.ticket_base);
       bend = bnext + B < p.Kw_active ? bnext + B : (bnext < p.Kw_active ? p.Kw_active : bnext + 1);
     }
     return bnext++;
@@ -546,14 +546,15 @@ cudaError_t launch_wadg_NC(const StageParams& p, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM_BYTES);
     grid_cap = sms * (per_sm > 0 ? per_sm : 1);
   }
-  if (p.Kw_active == 0) return cudaSuccess;
-  const long long need = (p.Kw_active + C::TPB - 1) / C::TPB;
+  const long long nact = p.Kw_active - p.Kw_begin; // elements of this launch
+  if (nact <= 0) return cudaSuccess;
+  const long long need = (nact + C::TPB - 1) / C::TPB;
   const int grid = (int)(need < grid_cap ? need : grid_cap);
   StageParams q = p;
   q.ticket_base = *p.ticket_host_next;
   q.ticket_batch = ticket_batch(N);
   const unsigned long long B = (unsigned long long)q.ticket_batch;
-  *p.ticket_host_next += B * (((unsigned long long)p.Kw_active + B - 1) / B + (unsigned long long)grid * C::TPB);
+  *p.ticket_host_next += B * (((unsigned long long)nact + B - 1) / B + (unsigned long long)grid * C::TPB);
   kern<<<grid, C::THREADS, C::SMEM_BYTES, s>>>(q);
   return cudaGetLastError();
 }

@@ -6,10 +6,12 @@ non-goal); this module implements the north star's sharding:
 * every element is owned by exactly one rank;
 * a rank's local mesh holds its owned elements plus the ghost layer, i.e.
   every non-owned element that shares a face with an owned one;
-* before each LSERK stage a rank receives the current states of its ghosts
-  from their owners.  Owned elements then see exactly the neighbour data of
-  the single-domain run, so their RHS (and therefore the time-stepping) is the
-  same as the global one (tests/test_partition.py checks this with gloo).
+* before each LSERK stage a rank receives, from their owners, the current
+  face traces (4 fields x face nodes) of its ghosts on the faces they share
+  with its owned elements -- the only ghost data the RHS reads (`trace_plan`).
+  Owned elements then see exactly the neighbour data of the single-domain
+  run, so their RHS (and therefore the time-stepping) is the same as the
+  global one (tests/test_partition.py checks this bit for bit with gloo).
 
 Two partitioners are provided:
 * `partition_mesh` -- generic: contiguous ranges of a Morton order of element
@@ -187,3 +189,39 @@ def layered_slab(surface_n: int, slab_interfaces, slab_sublayers, slab_media, nr
         part.send[rank + 1] = top_owned * ntri + tri_ids
         part.recv[rank + 1] = (nlocal - 1) * ntri + tri_ids
     return part
+
+
+def face_offsets(disc) -> np.ndarray:
+    """start of each element's faces in the (element, face) tables (wedges 5, tets 4)."""
+    nw, nt = int(disc.info.num_wedges), int(disc.info.num_tets)
+    return np.concatenate([5 * np.arange(nw + 1), 5 * nw + 4 * np.arange(1, nt + 1)]).astype(np.int64)
+
+
+def trace_plan(part: LocalPartition, disc):
+    """Face-trace exchange plan: peer -> (local elements, faces) to send / receive.
+
+    Send to q: faces of my owned elements in part.send[q] whose neighbour is a
+    ghost I receive from q.  Receive from q: faces of my ghosts in part.recv[q]
+    whose neighbour I own.  Both ranks enumerate the same physical faces in the
+    same order (element lists are identically ordered, element-local face
+    numbering is the global one), so the per-face trace lists align."""
+    nbr, _, _ = disc.face_table()
+    off = face_offsets(disc)
+    out = {"send": {}, "recv": {}}
+    for q in sorted(set(part.send) | set(part.recv)):
+        ghost_from_q = np.zeros(len(part.owned), dtype=bool)
+        if q in part.recv:
+            ghost_from_q[part.recv[q]] = True
+        for kind, ids, want in (("send", part.send.get(q), lambda nb: ghost_from_q[nb]),
+                                ("recv", part.recv.get(q), lambda nb: part.owned[nb] != 0)):
+            if ids is None:
+                continue
+            elems, faces = [], []
+            for e in ids.tolist():
+                for f in range(off[e + 1] - off[e]):
+                    nb = nbr[off[e] + f]
+                    if nb >= 0 and want(nb):
+                        elems.append(e)
+                        faces.append(f)
+            out[kind][q] = (np.array(elems, dtype=np.int64), np.array(faces, dtype=np.int32))
+    return out

@@ -53,20 +53,55 @@ def exchange(u, off, part):
         u[np.concatenate(blocks)] = buf.numpy()
 
 
-def run_rank(rank, world, port, case, degree, nsteps, out_dir):
+def trace_index(d, plan_side):
+    """reference-layout state offsets of the face traces of (element, face) pairs"""
+    off = d.elem_offset()
+    out = []
+    for e, f in zip(*plan_side):
+        my, _ = d.face_nodes(int(e), int(f))
+        npe = (off[e + 1] - off[e]) // 4
+        for fld in range(4):
+            out.append(off[e] + fld * npe + np.asarray(my, dtype=np.int64))
+    return np.concatenate(out) if out else np.zeros(0, np.int64)
+
+
+def exchange_traces(u, plan):
+    """face-trace refresh over gloo (what the GPU path ships): only the shared faces"""
+    import torch
+    reqs, bufs = [], {}
+    for q in sorted(set(plan["send_idx"]) | set(plan["recv_idx"])):
+        if q in plan["send_idx"]:
+            reqs.append(dist.isend(torch.from_numpy(u[plan["send_idx"][q]].copy()), q))
+        if q in plan["recv_idx"]:
+            bufs[q] = torch.zeros(len(plan["recv_idx"][q]), dtype=torch.float64)
+            reqs.append(dist.irecv(bufs[q], q))
+    for r in reqs:
+        r.wait()
+    for q, buf in bufs.items():
+        u[plan["recv_idx"][q]] = buf.numpy()
+
+
+def run_rank(rank, world, port, case, degree, nsteps, out_dir, mode="elements"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         part = make_partition(case, world, rank)
         d = pdg.build_discretization(part.mesh, degree)
         off = d.elem_offset()
+        if mode == "traces":
+            tp = P.trace_plan(part, d)
+            plan = {"send_idx": {q: trace_index(d, v) for q, v in tp["send"].items()},
+                    "recv_idx": {q: trace_index(d, v) for q, v in tp["recv"].items()}}
         u = pdg.make_initial_state(d, "gaussian", [0.35, 0.1, -0.05, 0.2]).u
         dt = 0.01
         res = np.zeros_like(u)
         owned_idx = np.concatenate(element_blocks(off, np.nonzero(part.owned)[0]))
         for _ in range(nsteps):
             for s in range(5):
-                exchange(u, off, part)
+                if mode == "traces":
+                    exchange_traces(u, plan)
+                else:
+                    exchange(u, off, part)
                 r = ob.rhs(d, u, threads=1)
                 res[owned_idx] = LSERK_A[s] * res[owned_idx] + dt * r[owned_idx]
                 u[owned_idx] += LSERK_B[s] * res[owned_idx]
@@ -95,10 +130,13 @@ def global_mesh(case, world):
     return P.layered_global(4, [-1.0, 0.0, 1.0], [2, 3], [(1.0, 1.0), (1.0, 4.0)], world)
 
 
-@pytest.mark.parametrize("case", ["hybrid", "unstructured", "layered"])
-def test_two_rank_lserk_matches_single_domain(case, tmp_path):
+@pytest.mark.parametrize("case,mode", [("hybrid", "elements"), ("unstructured", "elements"), ("layered", "elements"),
+                                       ("hybrid", "traces"), ("unstructured", "traces"), ("layered", "traces")])
+def test_two_rank_lserk_matches_single_domain(case, mode, tmp_path):
+    """Whole-element ghost refresh and face-trace-only refresh (the GPU path's) both
+    reproduce the single-domain run bit for bit: the RHS reads nothing else of a ghost."""
     world, degree, nsteps = 2, 2, 3
-    mp.spawn(run_rank, args=(world, free_port(), case, degree, nsteps, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(run_rank, args=(world, free_port(), case, degree, nsteps, str(tmp_path), mode), nprocs=world, join=True)
     d = pdg.build_discretization(global_mesh(case, world), degree)
     ug = pdg.make_initial_state(d, "gaussian", [0.35, 0.1, -0.05, 0.2]).u
     res = np.zeros_like(ug)
@@ -133,3 +171,20 @@ def test_partition_plans_are_consistent():
             assert np.array_equal(p.local_to_global[ids], parts[q].local_to_global[parts[q].recv[p.rank]])
             assert np.all(p.owned[ids] == 1)
             assert np.all(parts[q].owned[parts[q].recv[p.rank]] == 0)
+
+
+def test_trace_plans_align_and_are_smaller():
+    mesh = pdg.structured_hybrid_box(3, 3, 2, 2)
+    world = 3
+    parts = [P.partition_mesh(mesh, world, r) for r in range(world)]
+    discs = [pdg.build_discretization(p.mesh, 3) for p in parts]
+    plans = [P.trace_plan(p, d) for p, d in zip(parts, discs)]
+    for p, d, pl in zip(parts, discs, plans):
+        for q, (elems, faces) in pl["send"].items():
+            re, rf = plans[q]["recv"][p.rank]
+            # same global elements and faces, in the same order, on both sides
+            assert np.array_equal(p.local_to_global[elems], parts[q].local_to_global[re])
+            assert np.array_equal(faces, rf)
+            assert len(trace_index(d, (elems, faces))) == len(trace_index(discs[q], (re, rf)))
+            whole = sum((d.elem_offset()[e + 1] - d.elem_offset()[e]) for e in p.send[q])
+            assert len(trace_index(d, (elems, faces))) < whole
