@@ -67,8 +67,10 @@ __host__ __device__ constexpr int slot_stride(int x, int NT) {
 #ifndef PDG_SIMT_THREADS
 #define PDG_SIMT_THREADS 128
 #endif
+// minimum resident CTAs per SM (register budget): 3 at N = 1 (measured faster),
+// 1 above (spills), profiles/round1_simt_variants_ab.txt
 #ifndef PDG_SIMT_MINB
-#define PDG_SIMT_MINB 1
+#define PDG_SIMT_MINB(N) ((N) == 1 ? 3 : 1)
 #endif
 
 template <int N, bool WADG = false>
@@ -127,7 +129,7 @@ __device__ __forceinline__ void load_chunk(const StageParams& p, double* stg, lo
 }
 
 template <int N, bool WADG>
-__global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB) wedge_simt_kernel(const StageParams p) {
+__global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB(N)) wedge_simt_kernel(const StageParams p) {
   using C = SCfg<N, WADG>;
   constexpr int NQ = C::NQ, NT = C::NT, NP = C::NP, FW = C::FW, WG = C::WG, E = C::E;
   constexpr int SU = C::SU, SG = C::SG, SF = C::SF, SV = C::SV;
@@ -229,6 +231,8 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB) wedge_s
 #pragma unroll
         for (int k = 0; k < NT; ++k) Lr[k] = __ldcs(L + k * NT);
       }
+      // early: loading the residual in the epilogue exposes its HBM latency
+      // (2x slower, profiles/round1_simt_variants_ab.txt)
 #pragma unroll
       for (int f = 0; f < 4; ++f)
 #pragma unroll
