@@ -58,6 +58,17 @@ def load_traffic(kind, degree):
         return None
 
 
+DMMA_PEAK_TFLOPS = 37.0  # measured FP64 tensor-core throughput on this B200 pool (scripts/micro/dmma_bench.cu)
+
+
+def wadg_flops_per_wedge_stage(N):
+    """algorithmic FP64 flops of the WADG stage kernel per wedge:
+    Ltilde formation, K-folded gradients, vertical terms, quad-face lifts, Ltilde B."""
+    nq, nt, nc = N + 1, (N + 1) * (N + 2) // 2, (N + 2) ** 2
+    return (2 * nt * nc * nt + 2 * 4 * nt * nt * nq + 4 * 2 * nt * nq * nq + 3 * 2 * 2 * nt * nq * nq
+            + 2 * nt * nt * 4 * nq)
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -243,6 +254,15 @@ def measure_degree(args, degree, ws, rank, local, peaks, with_e2e=True):
         "tets": mesh.num_tets(),
         "clocks": clk.summary(),
     }
+    if mass == "wadg" and mesh.num_tets() == 0:
+        # WADG trades the streamed operators for FP64 tensor work: report
+        # the FP64 DMMA pipe roofline beside the HBM one (algorithmic flops, DESIGN 3.3)
+        fl = wadg_flops_per_wedge_stage(degree) * mesh.num_wedges()
+        res["tensor_roofline"] = {"bound": "tensor", "achieved": fl / (wedge_avg_ms / 1e3) / 1e12,
+                                  "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                  "frac": fl / (wedge_avg_ms / 1e3) / 1e12 / DMMA_PEAK_TFLOPS,
+                                  "peak_source": "FP64 mma.sync m8n8k4 (DMMA), scripts/micro/dmma_bench.cu on this pool",
+                                  "flops_per_launch": fl}
     if mesh.num_tets() > 0:
         t_ach = tbytes / (tet_avg_ms / 1e3) / 1e9
         res["tet_kernel_avg_ms"] = tet_avg_ms
@@ -334,7 +354,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--degree", type=int, default=5)
-    ap.add_argument("--degrees", default="", help="comma list for the order sweep, e.g. 1,2,3,4,5,6,7")
+    ap.add_argument("--degrees", default="1,2,3,4,6,7",
+                    help="comma list for the order sweep reported under 'sweep' ('' = headline degree only)")
     ap.add_argument("--surface-n", type=int, default=100)
     ap.add_argument("--sublayers", default="15,15,20")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -385,7 +406,7 @@ def main():
             continue
         r = measure_degree(args, deg, ws, rank, local, peaks, with_e2e=False)
         sweep.append({k: r[k] for k in ("degree", "value", "ms_per_step", "wedge_kernel_avg_ms", "roofline",
-                                        "total_dofs", "setup_s", "gpu_launches")})
+                                        "total_dofs", "setup_s", "gpu_launches", "tensor_roofline") if k in r})
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -410,7 +431,8 @@ def main():
             "roofline": head["roofline"], "cpu_baseline": cpu, "e2e": head.get("e2e"),
             "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
             "wedge_kernel_avg_ms": head["wedge_kernel_avg_ms"], "wedge_kernel_share": head["wedge_kernel_share"],
-            **({k: head[k] for k in ("tet_kernel_avg_ms", "tet_kernel_share", "tet_roofline") if k in head}),
+            **({k: head[k] for k in ("tet_kernel_avg_ms", "tet_kernel_share", "tet_roofline", "tensor_roofline")
+                if k in head}),
             "setup_s": head["setup_s"],
         }
         if sweep:

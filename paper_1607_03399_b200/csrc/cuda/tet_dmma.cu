@@ -37,6 +37,14 @@ __host__ __device__ constexpr int cf_stride(int x) {
 }
 
 constexpr int kTB = 8; // tets per batch (the N dimension of every product)
+// CTA size cap and stage depth: 640 / double-buffered measured best at N = 4
+// (single-buffered 480/640-thread variants spill: 1.92 / 2.13 vs 1.65 ms)
+#ifndef PDG_TET_CAP
+#define PDG_TET_CAP 640 // threads per CTA
+#endif
+#ifndef PDG_TET_STAGES
+#define PDG_TET_STAGES 2
+#endif
 constexpr int kComboCapT = 2048; // ints of neighbour node maps kept in shared memory
 
 template <int N, int NST_>
@@ -63,7 +71,7 @@ struct TDCfg {
   static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 4 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
   static constexpr int PER_TEAM = 4 + NSTAGE * STAGE + WORK;
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
-  static constexpr int TPB = cmax(1, cmin(cmin(8, 640 / (32 * T)), TPB_SMEM));
+  static constexpr int TPB = cmax(1, cmin(cmin(8, PDG_TET_CAP / (32 * T)), TPB_SMEM));
   static constexpr int THREADS = 32 * T * TPB;
   static constexpr size_t SMEM_BYTES = (size_t)8 * (TABLES + TPB * PER_TEAM);
   static_assert(VST >= 4 * KS && FST >= 4 * KF, "padded K ranges must fit the column strides");
@@ -353,7 +361,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
 
 template <int N>
 cudaError_t launch_tet_dmma_N(const StageParams& p, cudaStream_t s) {
-  using C = TDCfg<N, 2>;
+  using C = TDCfg<N, PDG_TET_STAGES>;
   constexpr int NST = C::NSTAGE;
   static int grid_cap = 0;
   auto kern = tet_dmma_kernel<N, NST>;
