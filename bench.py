@@ -59,6 +59,7 @@ def load_traffic(kind, degree):
 
 
 DMMA_PEAK_TFLOPS = 37.0  # measured FP64 tensor-core throughput on this B200 pool (scripts/micro/dmma_bench.cu)
+DFMA_PEAK_TFLOPS = 33.0  # measured FP64 FMA (CUDA-core) throughput, same microbenchmark
 
 
 def wadg_flops_per_wedge_stage(N):
@@ -258,10 +259,12 @@ def measure_degree(args, degree, ws, rank, local, peaks, with_e2e=True):
         # WADG trades the streamed operators for FP64 tensor work: report
         # the FP64 DMMA pipe roofline beside the HBM one (algorithmic flops, DESIGN 3.3)
         fl = wadg_flops_per_wedge_stage(degree) * mesh.num_wedges()
-        res["tensor_roofline"] = {"bound": "tensor", "achieved": fl / (wedge_avg_ms / 1e3) / 1e12,
-                                  "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                                  "frac": fl / (wedge_avg_ms / 1e3) / 1e12 / DMMA_PEAK_TFLOPS,
-                                  "peak_source": "FP64 mma.sync m8n8k4 (DMMA), scripts/micro/dmma_bench.cu on this pool",
+        simt = degree <= 3  # the low-order WADG kernel runs on the FP64 CUDA cores
+        pk = DFMA_PEAK_TFLOPS if simt else DMMA_PEAK_TFLOPS
+        res["tensor_roofline"] = {"bound": "fp64" if simt else "tensor", "achieved": fl / (wedge_avg_ms / 1e3) / 1e12,
+                                  "peak": pk, "unit": "TFLOP/s", "frac": fl / (wedge_avg_ms / 1e3) / 1e12 / pk,
+                                  "peak_source": ("FP64 FMA" if simt else "FP64 mma.sync m8n8k4 (DMMA)") +
+                                                 ", scripts/micro/dmma_bench.cu on this pool",
                                   "flops_per_launch": fl}
     if mesh.num_tets() > 0:
         t_ach = tbytes / (tet_avg_ms / 1e3) / 1e9
