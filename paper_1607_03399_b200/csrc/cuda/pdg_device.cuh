@@ -16,6 +16,7 @@
 namespace pdg {
 
 constexpr int kMaxN = 9;
+constexpr int kMaxDevices = 64; // per-device launch-configuration caches
 
 __host__ __device__ constexpr int nq_of(int N) { return N + 1; }
 __host__ __device__ constexpr int nt_of(int N) { return (N + 1) * (N + 2) / 2; }

@@ -363,21 +363,24 @@ template <int N>
 cudaError_t launch_tet_dmma_N(const StageParams& p, cudaStream_t s) {
   using C = TDCfg<N, PDG_TET_STAGES>;
   constexpr int NST = C::NSTAGE;
-  static int grid_cap = 0;
+  // one-time setup per device (the smem attribute is per device)
+  static int grid_cap[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
   auto kern = tet_dmma_kernel<N, NST>;
-  if (grid_cap == 0) {
+  if (grid_cap[dev] == 0) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
     if (err != cudaSuccess) return err;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
+    int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM_BYTES);
-    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+    grid_cap[dev] = sms * (per_sm > 0 ? per_sm : 1);
   }
   if (p.Kt_active - p.Kt_begin <= 0) return cudaSuccess;
   const long long nbatch = (p.Kt_active - p.Kt_begin + kTB - 1) / kTB;
   const long long need = (nbatch + C::TPB - 1) / C::TPB;
-  const int grid = (int)(need < grid_cap ? need : grid_cap);
+  const int grid = (int)(need < grid_cap[dev] ? need : grid_cap[dev]);
   StageParams q = p;
   q.ticket_base = *p.ticket_host_next;
   *p.ticket_host_next += (unsigned long long)nbatch + (unsigned long long)grid * C::TPB;

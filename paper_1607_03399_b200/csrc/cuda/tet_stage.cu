@@ -172,13 +172,16 @@ tet_stage_kernel(const StageParams p) {
 template <int N>
 cudaError_t launch_tet_N(const StageParams& p, cudaStream_t s) {
   using C = TCfg<N>;
-  static bool configured = false;
-  if (!configured) {
+  static bool configured[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
+  if (!configured[dev]) {
     cudaError_t err = cudaFuncSetAttribute(tet_stage_kernel<N>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)C::SMEM_BYTES);
     if (err != cudaSuccess) return err;
-    configured = true;
+    configured[dev] = true;
   }
   if (p.Kt_active - p.Kt_begin <= 0) return cudaSuccess;
   const long long blocks = (p.Kt_active - p.Kt_begin + C::E - 1) / C::E;

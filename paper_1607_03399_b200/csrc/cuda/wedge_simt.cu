@@ -583,20 +583,23 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB(N)) wedg
 template <int N, bool WADG>
 cudaError_t launch_simt_N(const StageParams& p, cudaStream_t s) {
   using C = SCfg<N, WADG>;
-  static int grid_cap = 0;
+  // one-time setup per device (the smem attribute is per device)
+  static int grid_cap[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
   auto kern = wedge_simt_kernel<N, WADG>;
-  if (grid_cap == 0) {
+  if (grid_cap[dev] == 0) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
     if (err != cudaSuccess) return err;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
+    int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM_BYTES);
-    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+    grid_cap[dev] = sms * (per_sm > 0 ? per_sm : 1);
   }
   if (p.Kw_active - p.Kw_begin <= 0) return cudaSuccess;
   const long long nchunk = (p.Kw_active - p.Kw_begin + C::E - 1) / C::E;
-  const int grid = (int)(nchunk < grid_cap ? nchunk : grid_cap);
+  const int grid = (int)(nchunk < grid_cap[dev] ? nchunk : grid_cap[dev]);
   StageParams q = p;
   q.ticket_base = *p.ticket_host_next;
   // every CTA grabs until it gets two tickets past the end (one in flight)

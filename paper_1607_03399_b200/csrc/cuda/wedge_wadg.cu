@@ -535,21 +535,24 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
 template <int N, bool CS, bool FUSED, int NST, bool TG>
 cudaError_t launch_wadg_NC(const StageParams& p, cudaStream_t s) {
   using C = WCfg<N, NST, TG>;
-  static int grid_cap = 0;
+  // one-time setup per device (the smem attribute is per device)
+  static int grid_cap[kMaxDevices] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
   auto kern = wedge_wadg_kernel<N, CS, FUSED, C::NSTAGE, TG>;
-  if (grid_cap == 0) {
+  if (grid_cap[dev] == 0) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
     if (err != cudaSuccess) return err;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
+    int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM_BYTES);
-    grid_cap = sms * (per_sm > 0 ? per_sm : 1);
+    grid_cap[dev] = sms * (per_sm > 0 ? per_sm : 1);
   }
   const long long nact = p.Kw_active - p.Kw_begin; // elements of this launch
   if (nact <= 0) return cudaSuccess;
   const long long need = (nact + C::TPB - 1) / C::TPB;
-  const int grid = (int)(need < grid_cap ? need : grid_cap);
+  const int grid = (int)(need < grid_cap[dev] ? need : grid_cap[dev]);
   StageParams q = p;
   q.ticket_base = *p.ticket_host_next;
   q.ticket_batch = ticket_batch(N);
