@@ -69,8 +69,15 @@ __host__ __device__ constexpr int slot_stride(int x, int NT) {
 #endif
 // minimum resident CTAs per SM (register budget): 3 at N = 1 (measured faster),
 // 1 above (spills), profiles/round1_simt_variants_ab.txt
+#ifndef PDG_SIMT_LATE_OPS
+#define PDG_SIMT_LATE_OPS 1
+#endif
 #ifndef PDG_SIMT_MINB
+#ifdef PDG_SIMT_MINB_ALL
+#define PDG_SIMT_MINB(N) (PDG_SIMT_MINB_ALL)
+#else
 #define PDG_SIMT_MINB(N) ((N) == 1 ? 3 : 1)
+#endif
 #endif
 
 template <int N, bool WADG = false>
@@ -225,20 +232,24 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB(N)) wedg
 
     // per-thread operands from HBM: row i of L, rows i of the quad lifts, residual
     double Lr[NT], rres[4][NQ];
-    if (active) {
-      if (!WADG) {
-        const double* L = p.Lt + ge * lcomp_of(N) + i;
+    auto load_operands = [&]() {
+      if (active) {
+        if (!WADG) {
+          const double* L = p.Lt + ge * lcomp_of(N) + i;
 #pragma unroll
-        for (int k = 0; k < NT; ++k) Lr[k] = __ldcs(L + k * NT);
+          for (int k = 0; k < NT; ++k) Lr[k] = __ldcs(L + k * NT);
+        }
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+          for (int j = 0; j < NQ; ++j)
+            rres[f][j] = res_src ? __ldcs(res_src + ge * 4 * NP + f * NP + j * NT + i) : 0.0;
       }
-      // early: loading the residual in the epilogue exposes its HBM latency
-      // (2x slower, profiles/round1_simt_variants_ab.txt)
-#pragma unroll
-      for (int f = 0; f < 4; ++f)
-#pragma unroll
-        for (int j = 0; j < NQ; ++j)
-          rres[f][j] = res_src ? __ldcs(res_src + ge * 4 * NP + f * NP + j * NT + i) : 0.0;
-    }
+    };
+    // per-thread operands from HBM (row i of L, residual): issued before the
+    // flux phase, or (PDG_SIMT_LATE_OPS) right after the flux arithmetic so the
+    // gathered traces and these registers are not live at the same time
+    if (!PDG_SIMT_LATE_OPS) load_operands();
 
     // ---- numerical fluxes of the chunk -------------------------------------------
     if (surf) {
@@ -307,6 +318,7 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB(N)) wedg
         }
       }
     }
+    if (PDG_SIMT_LATE_OPS) load_operands();
     if (WADG)
       for (int q = threadIdx.x; q < nel * C::NC; q += C::THREADS) {
         const int e = q / C::NC, qq = q - e * C::NC;
