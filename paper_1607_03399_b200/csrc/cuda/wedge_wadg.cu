@@ -46,6 +46,11 @@ __host__ __device__ constexpr int cf_stride(int x) {
 }
 
 constexpr int kComboCapW = 2048; // ints of neighbour node maps kept in shared memory
+// threads per CTA: 384 (>= 168 registers) at N <= 6, 512 at N = 7 (global tables)
+// -- measured, profiles/round1_wadg_tables.txt
+#ifndef PDG_WADG_THREAD_CAP
+#define PDG_WADG_THREAD_CAP(N) ((N) >= 7 ? 512 : 384)
+#endif
 
 template <int N, int NST_, bool TG = false>
 struct WCfg {
@@ -78,7 +83,7 @@ struct WCfg {
   static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 6 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
   static constexpr int PER_TEAM = 6 + NSTAGE * STAGE + WORK;
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
-  static constexpr int TPB = cmax(1, cmin(cmin(15, 512 / (32 * T)), TPB_SMEM)); // teams per CTA
+  static constexpr int TPB = cmax(1, cmin(cmin(15, PDG_WADG_THREAD_CAP(N) / (32 * T)), TPB_SMEM)); // teams per CTA
   static constexpr int THREADS = 32 * T * TPB;
   static constexpr size_t SMEM_BYTES = (size_t)8 * (TABLES + TPB * PER_TEAM);
   static constexpr int QF_LANE = ceil_div(FW, 32 * T); // face nodes per team thread
