@@ -39,8 +39,10 @@ __host__ __device__ constexpr int cf_stride(int x) {
 constexpr int kTB = 8; // tets per batch (the N dimension of every product)
 // CTA size cap and stage depth: 640 / double-buffered measured best at N = 4
 // (single-buffered 480/640-thread variants spill: 1.92 / 2.13 vs 1.65 ms)
+// threads per CTA (register budget): 400 at N = 3, 640 otherwise (measured:
+// N=3 0.97 vs 1.11 ms, N=4 1.65 vs 1.75 ms for 400)
 #ifndef PDG_TET_CAP
-#define PDG_TET_CAP 640 // threads per CTA
+#define PDG_TET_CAP(N) ((N) == 3 ? 400 : 640)
 #endif
 #ifndef PDG_TET_STAGES
 #define PDG_TET_STAGES 2
@@ -71,7 +73,7 @@ struct TDCfg {
   static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 4 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
   static constexpr int PER_TEAM = 4 + NSTAGE * STAGE + WORK;
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
-  static constexpr int TPB = cmax(1, cmin(cmin(8, PDG_TET_CAP / (32 * T)), TPB_SMEM));
+  static constexpr int TPB = cmax(1, cmin(cmin(8, PDG_TET_CAP(N) / (32 * T)), TPB_SMEM));
   static constexpr int THREADS = 32 * T * TPB;
   static constexpr size_t SMEM_BYTES = (size_t)8 * (TABLES + TPB * PER_TEAM);
   static_assert(VST >= 4 * KS && FST >= 4 * KF, "padded K ranges must fit the column strides");
