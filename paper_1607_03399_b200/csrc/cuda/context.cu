@@ -175,6 +175,7 @@ StageParams base_params(pdg_ctx* c) {
   p.tDtT = c->tDtT;
   p.tLiftT = c->tLiftT;
   p.tface = c->tface;
+  p.tet_frag = c->tet_frag;
   p.nbr_nodes = c->nbr_nodes;
   p.max_nfp = c->max_nfp;
   p.nbr_nodes_len = c->nbr_nodes_len;
@@ -518,6 +519,11 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags,
       c->w1d = upload(w1d);
       c->Mtet = upload(Mtet);
     }
+    if (c->Kt > 0 && tet_frag_size(N) > 0) {
+      c->tet_frag = dalloc<double>(tet_frag_size(N));
+      StageParams tp = base_params(c);
+      PDG_CK(launch_tet_frag_fill(N, tp, c->tet_frag, c->stream));
+    }
 
     // ---- state buffers --------------------------------------------------------
     const std::size_t nd = (std::size_t)c->total_dofs;
@@ -560,7 +566,7 @@ void destroy_context(pdg_ctx* c) {
     cudaEventDestroy(pe.a);
     cudaEventDestroy(pe.b);
   }
-  void* ptrs[] = {c->u[0], c->u[1], c->res, c->rhs, c->stage, c->wgeo, c->wconn, c->Lt, c->QL, c->wadg, c->wadg_frag,
+  void* ptrs[] = {c->u[0], c->u[1], c->res, c->rhs, c->stage, c->wgeo, c->wconn, c->Lt, c->QL, c->wadg, c->wadg_frag, c->tet_frag,
                   c->tgeo, c->tconn, c->DrT, c->DsT, c->Dt, c->prof, c->wface_dev, c->tDrT,
                   c->tDsT, c->tDtT, c->tLiftT, c->tface, c->nbr_nodes, c->Mtri, c->Xr, c->Xs,
                   c->M1D, c->w1d, c->Mtet, c->partials, c->scalar, c->badflag, c->ticket, c->dev_to_ref,

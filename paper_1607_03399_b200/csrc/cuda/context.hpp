@@ -36,6 +36,7 @@ struct pdg_ctx {
   double* QL = nullptr;
   double* wadg = nullptr; // WADG shared tables (mass_mode == wadg)
   double* wadg_frag = nullptr; // fragment-major copy of the big WADG tables
+  double* tet_frag = nullptr;  // fragment-major tet operators (N >= 6, read from L2/L1)
   bool wedge_simt = false; // low-order CUDA-core wedge kernel (compact L / quad-lift layout)
   double* tgeo = nullptr;
   int* tconn = nullptr;

@@ -119,6 +119,7 @@ struct StageParams {
   const double* __restrict__ tDtT;
   const double* __restrict__ tLiftT; // [4*nt][n]
   const int* __restrict__ tface; // [4*nt] tet face nodes
+  const double* __restrict__ tet_frag; // fragment-major tet operators in global memory (N >= 6)
   const int* __restrict__ nbr_nodes; // [combo][max_nfp]
   int max_nfp;
   int nbr_nodes_len; // ints in nbr_nodes
@@ -153,7 +154,9 @@ int wedge_simt_max_degree();
 cudaError_t launch_wedge_simt_stage(int N, const StageParams& p, cudaStream_t s); // low-order CUDA-core wedge kernel
 int wedge_wadg_simt_max_degree();
 cudaError_t launch_wedge_wadg_simt_stage(int N, const StageParams& p, cudaStream_t s); // low-order WADG
-cudaError_t launch_tet_dmma_stage(int N, const StageParams& p, cudaStream_t s); // batched DMMA tet kernel (N <= 5)
+cudaError_t launch_tet_dmma_stage(int N, const StageParams& p, cudaStream_t s); // batched DMMA tet kernel (N <= 7)
+size_t tet_frag_size(int N);
+cudaError_t launch_tet_frag_fill(int N, const StageParams& p, double* out, cudaStream_t s);
 cudaError_t launch_wedge_wadg_stage(int N, const StageParams& p, cudaStream_t s); // WADG (DMMA) kernel
 size_t wadg_frag_size(int N);
 cudaError_t launch_wadg_frag_fill(int N, const double* wadg, double* out, cudaStream_t s);

@@ -42,12 +42,18 @@ constexpr int kTB = 8; // tets per batch (the N dimension of every product)
 // threads per CTA (register budget): 400 at N = 3, 640 otherwise (measured:
 // N=3 0.97 vs 1.11 ms, N=4 1.65 vs 1.75 ms for 400)
 #ifndef PDG_TET_CAP
-#define PDG_TET_CAP(N) ((N) == 3 ? 400 : 640)
+#define PDG_TET_CAP(N) ((N) == 3 ? 400 : ((N) >= 6 ? PDG_TET_CAP_HI : 640))
+#endif
+#ifndef PDG_TET_CAP_HI
+#define PDG_TET_CAP_HI 512
 #endif
 #ifndef PDG_TET_STAGES
 #define PDG_TET_STAGES 2
 #endif
 constexpr int kComboCapT = 2048; // ints of neighbour node maps kept in shared memory
+
+/// N >= 6: the operators (>= 0.25 MB) stay in L2/L1-resident global memory
+__host__ __device__ constexpr bool tet_tables_global(int N) { return N >= 6; }
 
 template <int N, int NST_>
 struct TDCfg {
@@ -58,7 +64,9 @@ struct TDCfg {
   static constexpr int T = IT;
   static constexpr int DTAB = IT * KS * 32;   // one of Dr, Ds, Dt
   static constexpr int LTAB = 4 * IT * KF * 32; // LIFT_f, f = 0..3
-  static constexpr int TABLES = r2(3 * DTAB + LTAB + ceil_div(4 * NT, 2) + kComboCapT / 2);
+  static constexpr int BIGTAB = 3 * DTAB + LTAB;
+  static constexpr bool TG = tet_tables_global(N);
+  static constexpr int TABLES = r2((TG ? 0 : BIGTAB) + ceil_div(4 * NT, 2) + kComboCapT / 2);
   static constexpr int VST = cf_stride(NP);   // B-buffer column stride (volume)
   static constexpr int FST = cf_stride(NT);   // flux-buffer column stride
   // per-stage buffers: state, records, connectivity of 8 tets (the residual
@@ -73,7 +81,7 @@ struct TDCfg {
   static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 4 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
   static constexpr int PER_TEAM = 4 + NSTAGE * STAGE + WORK;
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
-  static constexpr int TPB = cmax(1, cmin(cmin(8, PDG_TET_CAP(N) / (32 * T)), TPB_SMEM));
+  static constexpr int TPB = cmax(1, cmin(cmin(8, cmax(1, PDG_TET_CAP(N) / (32 * T))), TPB_SMEM));
   static constexpr int THREADS = 32 * T * TPB;
   static constexpr size_t SMEM_BYTES = (size_t)8 * (TABLES + TPB * PER_TEAM);
   static_assert(VST >= 4 * KS && FST >= 4 * KF, "padded K ranges must fit the column strides");
@@ -105,31 +113,48 @@ __device__ __forceinline__ void load_batch(const StageParams& p, double* stg, lo
   tma_load_1d_hint(G + kTB * kTG, p.tconn + t0 * 8, 32u * nel, bar, stream);
 }
 
+/// fragment-major operator tables [D_r | D_s | D_t][t][s][lane], LIFT_f [f][t][s][lane]
+template <int N>
+__device__ void fill_tet_tables(double* dst, const StageParams& p, int tid, int nthr) {
+  using C = TDCfg<N, 1>;
+  constexpr int NP = C::NP, NT = C::NT, IT = C::IT, KS = C::KS, KF = C::KF;
+  double* sD = dst;
+  double* sL = dst + 3 * C::DTAB;
+  for (int q = tid; q < 3 * C::DTAB; q += nthr) {
+    const int lane = q & 31, rest = q >> 5;
+    const int s = rest % KS, t = (rest / KS) % IT, a = rest / (KS * IT);
+    const int n = 8 * t + (lane >> 2), k = 4 * s + (lane & 3);
+    const double* src = a == 0 ? p.tDrT : (a == 1 ? p.tDsT : p.tDtT);
+    sD[q] = (n < NP && k < NP) ? src[k * NP + n] : 0.0;
+  }
+  for (int q = tid; q < C::LTAB; q += nthr) {
+    const int lane = q & 31, rest = q >> 5;
+    const int s = rest % KF, t = (rest / KF) % IT, f = rest / (KF * IT);
+    const int n = 8 * t + (lane >> 2), m = 4 * s + (lane & 3);
+    sL[q] = (n < NP && m < NT) ? p.tLiftT[(f * NT + m) * NP + n] : 0.0;
+  }
+}
+
+template <int N>
+__global__ void tet_frag_kernel(const StageParams p, double* out) {
+  fill_tet_tables<N>(out, p, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+}
+
 template <int N, int NST>
 __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(const StageParams p) {
   using C = TDCfg<N, NST>;
   constexpr int NP = C::NP, NT = C::NT, IT = C::IT, KS = C::KS, KF = C::KF, T = C::T;
   constexpr int VST = C::VST, FST = C::FST;
   extern __shared__ __align__(16) double smem[];
-  double* sD = smem;                    // [a][t][s][lane] = D_a(8t+gid, 4s+tig), a = r, s, t
-  double* sL = sD + 3 * C::DTAB;        // [f][t][s][lane] = LIFT(8t+gid, f NT + 4s+tig)
-  int* sFace = reinterpret_cast<int*>(sL + C::LTAB); // [4 NT] face node -> volume node
-  int* sCombo = sFace + 2 * ceil_div(4 * NT, 2);       // neighbour node maps (when they fit)
+  double* sSmall = smem + (C::TG ? 0 : C::BIGTAB);
+  int* sFace = reinterpret_cast<int*>(sSmall); // [4 NT] face node -> volume node
+  int* sCombo = sFace + 2 * ceil_div(4 * NT, 2); // neighbour node maps (when they fit)
   for (int q = threadIdx.x; q < (int)(C::SMEM_BYTES / 8); q += C::THREADS) smem[q] = 0.0;
   __syncthreads();
-  for (int q = threadIdx.x; q < 3 * C::DTAB; q += C::THREADS) {
-    const int lane = q & 31, rest = q >> 5;
-    const int s = rest % KS, t = (rest / KS) % IT, a = rest / (KS * IT);
-    const int n = 8 * t + (lane >> 2), k = 4 * s + (lane & 3);
-    const double* src = a == 0 ? p.tDrT : (a == 1 ? p.tDsT : p.tDtT);
-    if (n < NP && k < NP) sD[q] = src[k * NP + n];
-  }
-  for (int q = threadIdx.x; q < C::LTAB; q += C::THREADS) {
-    const int lane = q & 31, rest = q >> 5;
-    const int s = rest % KF, t = (rest / KF) % IT, f = rest / (KF * IT);
-    const int n = 8 * t + (lane >> 2), m = 4 * s + (lane & 3);
-    if (n < NP && m < NT) sL[q] = p.tLiftT[(f * NT + m) * NP + n];
-  }
+  if (!C::TG) fill_tet_tables<N>(smem, p, threadIdx.x, C::THREADS);
+  const double* sD = C::TG ? p.tet_frag : smem;   // [a][t][s][lane] = D_a(8t+gid, 4s+tig), a = r, s, t
+  const double* sL = sD + 3 * C::DTAB;             // [f][t][s][lane] = LIFT(8t+gid, f NT + 4s+tig)
+  auto tab = [](const double* t, int idx) -> double { return C::TG ? __ldg(t + idx) : t[idx]; };
   for (int q = threadIdx.x; q < 4 * NT; q += C::THREADS) sFace[q] = p.tface[q];
   const bool combo_smem = p.nbr_nodes_len <= kComboCapT;
   if (combo_smem)
@@ -286,7 +311,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
 #pragma unroll
       for (int s2 = 0; s2 < KS; ++s2) {
         const int fo = ((w * KS + s2) << 5) + lane;
-        const double ar = sD[fo], as = sD[C::DTAB + fo], at = sD[2 * C::DTAB + fo];
+        const double ar = tab(sD, fo), as = tab(sD, C::DTAB + fo), at = tab(sD, 2 * C::DTAB + fo);
         const int bo = gid * VST + 4 * s2 + tig;
         const double bp = BVb[bo];
         dmma(gr, ar, bp);
@@ -302,7 +327,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
       for (int f = 0; f < 4; ++f)
 #pragma unroll
         for (int s2 = 0; s2 < KF; ++s2) {
-          const double a = sL[(((f * IT + w) * KF + s2) << 5) + lane];
+          const double a = tab(sL, (((f * IT + w) * KF + s2) << 5) + lane);
           const int bo = (f * kTB + gid) * FST + 4 * s2 + tig;
           dmma(lp, a, FPb[bo]);
           dmma(lu[f], a, FUb[bo]);
@@ -392,12 +417,30 @@ cudaError_t launch_tet_dmma_N(const StageParams& p, cudaStream_t s) {
 
 } // namespace
 
-bool tet_dmma_supported(int N) { return N >= 1 && N <= 5; }
+bool tet_dmma_supported(int N) { return N >= 1 && N <= 7; }
+
+size_t tet_frag_size(int N) {
+  switch (N) {
+#define PDG_CASE(n) case n: return tet_tables_global(n) ? (size_t)TDCfg<n, 1>::BIGTAB : 0;
+    PDG_CASE(1) PDG_CASE(2) PDG_CASE(3) PDG_CASE(4) PDG_CASE(5) PDG_CASE(6) PDG_CASE(7)
+#undef PDG_CASE
+  }
+  return 0;
+}
+
+cudaError_t launch_tet_frag_fill(int N, const StageParams& p, double* out, cudaStream_t s) {
+  switch (N) {
+#define PDG_CASE(n) case n: tet_frag_kernel<n><<<64, 256, 0, s>>>(p, out); return cudaGetLastError();
+    PDG_CASE(6) PDG_CASE(7)
+#undef PDG_CASE
+  }
+  return cudaSuccess;
+}
 
 cudaError_t launch_tet_dmma_stage(int N, const StageParams& p, cudaStream_t s) {
   switch (N) {
 #define PDG_CASE(n) case n: return launch_tet_dmma_N<n>(p, s);
-    PDG_CASE(1) PDG_CASE(2) PDG_CASE(3) PDG_CASE(4) PDG_CASE(5)
+    PDG_CASE(1) PDG_CASE(2) PDG_CASE(3) PDG_CASE(4) PDG_CASE(5) PDG_CASE(6) PDG_CASE(7)
 #undef PDG_CASE
   }
   return cudaErrorInvalidValue;
