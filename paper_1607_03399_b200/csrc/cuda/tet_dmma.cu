@@ -53,7 +53,10 @@ constexpr int kTB = 8; // tets per batch (the N dimension of every product)
 constexpr int kComboCapT = 2048; // ints of neighbour node maps kept in shared memory
 
 /// N >= 6: the operators (>= 0.25 MB) stay in L2/L1-resident global memory
-__host__ __device__ constexpr bool tet_tables_global(int N) { return N >= 6; }
+#ifndef PDG_TET_TG_MIN_N
+#define PDG_TET_TG_MIN_N 5 // measured: N=5 3.79 -> 3.16 ms, N=4 1.65 -> 1.85 ms with global tables
+#endif
+__host__ __device__ constexpr bool tet_tables_global(int N) { return N >= PDG_TET_TG_MIN_N; }
 
 template <int N, int NST_>
 struct TDCfg {
@@ -430,8 +433,12 @@ size_t tet_frag_size(int N) {
 
 cudaError_t launch_tet_frag_fill(int N, const StageParams& p, double* out, cudaStream_t s) {
   switch (N) {
-#define PDG_CASE(n) case n: tet_frag_kernel<n><<<64, 256, 0, s>>>(p, out); return cudaGetLastError();
-    PDG_CASE(6) PDG_CASE(7)
+#define PDG_CASE(n) \
+  case n:           \
+    if (!tet_tables_global(n)) return cudaSuccess; \
+    tet_frag_kernel<n><<<64, 256, 0, s>>>(p, out); \
+    return cudaGetLastError();
+    PDG_CASE(1) PDG_CASE(2) PDG_CASE(3) PDG_CASE(4) PDG_CASE(5) PDG_CASE(6) PDG_CASE(7)
 #undef PDG_CASE
   }
   return cudaSuccess;
