@@ -60,6 +60,9 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #ifndef PDG_COMPACT_OPS
 #define PDG_COMPACT_OPS 1
 #endif
+#ifndef PDG_PAD_STATE
+#define PDG_PAD_STATE 1
+#endif
 #ifndef PDG_THREAD_CAP
 #define PDG_THREAD_CAP 384
 #endif
@@ -83,7 +86,13 @@ struct DCfg {
   static constexpr int FQ = 3 * JT * KT * 32;                // fragment-major quad fluxes
   static constexpr int FTRI = r2(4 * KS + NT + 8);           // bottom/top tri fluxes (+ padding)
   static constexpr int ZS = r2(4 * KS);                      // zero column for padded B reads
-  static constexpr int WORK = VS + 2 * (FTRI + FQ) + ZS;
+  // padded copy of the state for bank-conflict-free fragment loads when NT is
+  // not 4 or 12 mod 16 (row = field*NQ + slice, stride SP)
+  // measured: N = 4 3.93 vs 4.22 ms, N = 5 6.55 vs 6.31 ms (profiles/round1_pad_state_ab.txt)
+  static constexpr bool PAD = PDG_PAD_STATE && cf_stride(NT) != NT && N == 4;
+  static constexpr int SP = PAD ? cf_stride(NT) : NT;
+  static constexpr int UPS = PAD ? r2((4 * NQ + 8 * JT + 4 * KT) * SP + 4 * KS + 8) : 0;
+  static constexpr int WORK = VS + 2 * (FTRI + FQ) + ZS + UPS;
   static constexpr int TABLES = r2(2 * IT * KS * 32 + JT * KT * 32 + 2 * NQ + ceil_div(FW, 2) + kComboCap / 2);
   static constexpr int SMEM_BUDGET = 225 * 1024;
   // double-buffered stages unless even a single team would not fit
@@ -192,6 +201,8 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
   double* Fqp = Ftu + C::FTRI;  // quad-face fluxes, fragment-major [f][jt][s][lane]
   double* Fqu = Fqp + C::FQ;
   const double* Zero = Fqu + C::FQ; // ZS zeros, never written
+  double* Upad = Fqu + C::FQ + C::ZS; // padded state copy (C::PAD)
+  constexpr int SP = C::SP;
   if (tt == 0) {
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
@@ -297,6 +308,14 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
     }
     mbar_wait(bar + s, NST == 2 ? ((n >> 1) & 1) : (n & 1));
 
+    // ---- padded state copy (published by the flux barrier) ----------------------
+    if (C::PAD)
+      for (int q = tt; q < 4 * NP; q += 32 * T) {
+        const int row = q / NT, col = q - row * NT;
+        Upad[row * SP + col] = U[q];
+      }
+    const double* Us = C::PAD ? Upad : U; // state with row stride SP
+
     // ---- numerical fluxes on all face nodes -------------------------------------
     if (surf) {
       gather(Cn);
@@ -348,9 +367,9 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
           for (int s2 = 0; s2 < KT; ++s2) {
             const int l = 4 * s2 + tig;
             const double bd = sDt[((jt * KT + s2) << 5) + lane];
-            dmma(d, U[NP + l * NT + i], sx_ * bd);
-            dmma(d, U[2 * NP + l * NT + i], sy_ * bd);
-            dmma(d, U[3 * NP + l * NT + i], tzJ * bd);
+            dmma(d, Us[(NQ + l) * SP + i], sx_ * bd);
+            dmma(d, Us[(2 * NQ + l) * SP + i], sy_ * bd);
+            dmma(d, Us[(3 * NQ + l) * SP + i], tzJ * bd);
           }
         }
 #pragma unroll
@@ -371,7 +390,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
 #pragma unroll
       for (int jt = 0; jt < JTL; ++jt) {
         const int nc = 8 * jt + gid;
-        src[jt] = nc < NQ ? U + nc * NT : (nc == NQ ? Ftu : (nc == NQ + 1 ? Ftu + NT : Zero));
+        src[jt] = nc < NQ ? Us + nc * SP : (nc == NQ ? Ftu : (nc == NQ + 1 ? Ftu + NT : Zero));
       }
       double gx[JT][2], gy[JT][2], dvx[JT][2], dvy[JT][2], lv[JT][2], lp[JTL][2];
 #pragma unroll
@@ -404,8 +423,8 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
             if (vol) {
               dmma(gx[jt], cx, bp);
               dmma(gy[jt], cy, bp);
-              dmma(dvx[jt], cx, U[NP + jb * NT + k]);
-              dmma(dvy[jt], cy, U[2 * NP + jb * NT + k]);
+              dmma(dvx[jt], cx, Us[(NQ + jb) * SP + k]);
+              dmma(dvy[jt], cy, Us[(2 * NQ + jb) * SP + k]);
             }
             dmma(lv[jt], la, V[jb * VST + k]);
           }
@@ -468,7 +487,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
         for (int a = 0; a < 3; ++a) n_[f][a] = nrm[3 * f + a];
       // per-lane base offset of position (i, j = 2 tig); (jt, c, field) add constants
       const int lane_off = 2 * tig * NT + i;
-      const double* Ul = U + lane_off;
+      const double* Ul = Us + 2 * tig * SP + i; // padded rows: (field*NQ + j)*SP + i
       const double* Rl = R + lane_off;
       const long long gofs = e * 4 * NP + lane_off;
       double* resl = p.res + gofs;
@@ -503,13 +522,15 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
             }
             const double rv[4] = {rp, rux, ruy, ruz};
             constexpr int cst[2] = {0, NT};
+            constexpr int csp[2] = {0, SP};
 #pragma unroll
             for (int f = 0; f < 4; ++f) {
               const int o = f * NP + 8 * jt * NT + cst[c];
+              const int ou = (f * NQ + 8 * jt) * SP + csp[c];
               if (lserk) {
                 const double rr = first ? pdt * rv[f] : pa * Rl[o] + pdt * rv[f];
                 __stcs(resl + o, rr); // streaming stores: evict first
-                __stcs(uol + o, Ul[o] + pb * rr);
+                __stcs(uol + o, Ul[ou] + pb * rr);
               } else {
                 __stcs(rhsl + o, accum ? Rl[o] + rv[f] : rv[f]);
               }
