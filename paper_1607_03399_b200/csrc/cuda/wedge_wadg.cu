@@ -46,6 +46,9 @@ __host__ __device__ constexpr int cf_stride(int x) {
 }
 
 constexpr int kComboCapW = 2048; // ints of neighbour node maps kept in shared memory
+#ifndef PDG_WADG_PAD_STATE
+#define PDG_WADG_PAD_STATE 1
+#endif
 // threads per CTA: 384 (>= 168 registers) at N <= 6, 512 at N = 7 (global tables)
 // -- measured, profiles/round1_wadg_tables.txt
 #ifndef PDG_WADG_THREAD_CAP
@@ -78,7 +81,12 @@ struct WCfg {
   static constexpr int FQ = 3 * JT * KT * 32;                // fragment-major quad fluxes
   static constexpr int FTRI = r2(2 * NT);                    // bottom/top tri fluxes
   static constexpr int IJ = r2(4 * KQ);                      // 1/J at the cubature points
-  static constexpr int WORK = BS + 2 * (FTRI + FQ) + IJ;
+  // padded state copy for bank-conflict-free fragment loads (see wedge_dmma.cu)
+  // measured: N = 4 5.05 -> 4.60 ms, N = 5 8.59 -> 8.86 ms (profiles/round1_pad_state_ab.txt)
+  static constexpr bool PAD = PDG_WADG_PAD_STATE && cf_stride(NT) != NT && N == 4;
+  static constexpr int SP = PAD ? cf_stride(NT) : NT;
+  static constexpr int UPS = PAD ? r2((4 * NQ + 8 * JT + 4 * KT) * SP + 4 * KS + 8) : 0;
+  static constexpr int WORK = BS + 2 * (FTRI + FQ) + IJ + UPS;
   static constexpr int SMEM_BUDGET = 225 * 1024;
   static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 6 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
   static constexpr int PER_TEAM = 6 + NSTAGE * STAGE + WORK;
@@ -222,6 +230,8 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
   double* Fqp = Ftu + C::FTRI;        // [f][jt][s][lane]
   double* Fqu = Fqp + C::FQ;
   double* sIJ = Fqu + C::FQ;          // [4 KQ], zero beyond NC
+  double* Upad = sIJ + C::IJ;         // padded state copy (C::PAD)
+  constexpr int SP = C::SP;
   if (tt == 0) {
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
@@ -291,6 +301,13 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
     }
     mbar_wait(bar + s, NST == 2 ? ((n >> 1) & 1) : (n & 1));
     const double j0 = G[w_jac(N)], jr = G[w_jac(N) + 1], js = G[w_jac(N) + 2];
+
+    if (C::PAD)
+      for (int q = tt; q < 4 * NP; q += 32 * T) {
+        const int row = q / NT, col = q - row * NT;
+        Upad[row * SP + col] = U[q];
+      }
+    const double* Us = C::PAD ? Upad : U; // state with row stride SP, published by the flux barrier
 
     // ---- numerical fluxes on all face nodes; 1/J at the cubature points -------
     if (surf) {
@@ -389,11 +406,11 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
 #pragma unroll
         for (int jt = 0; jt < JT; ++jt) {
           const int jb = 8 * jt + gid;
-          const double bp = U[jb * NT + k];
+          const double bp = Us[jb * SP + k];
           dmma(gx[jt], ax, bp);
           dmma(gy[jt], ay, bp);
-          dmma(dvx[jt], ax, U[NP + jb * NT + k]);
-          dmma(dvy[jt], ay, U[2 * NP + jb * NT + k]);
+          dmma(dvx[jt], ax, Us[(NQ + jb) * SP + k]);
+          dmma(dvy[jt], ay, Us[(2 * NQ + jb) * SP + k]);
         }
       }
     }
@@ -413,10 +430,10 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
         for (int s2 = 0; s2 < KT; ++s2) {
           const int l = 4 * s2 + tig;
           const double bd = sDt[((jt * KT + s2) << 5) + lane];
-          dmma(vp[jt], U[NP + l * NT + i], sx_ * bd);
-          dmma(vp[jt], U[2 * NP + l * NT + i], sy_ * bd);
-          dmma(vp[jt], U[3 * NP + l * NT + i], tzJ * bd);
-          dmma(pdt[jt], U[l * NT + i], bd);
+          dmma(vp[jt], Us[(NQ + l) * SP + i], sx_ * bd);
+          dmma(vp[jt], Us[(2 * NQ + l) * SP + i], sy_ * bd);
+          dmma(vp[jt], Us[(3 * NQ + l) * SP + i], tzJ * bd);
+          dmma(pdt[jt], Us[l * SP + i], bd);
         }
       }
     }
@@ -524,7 +541,7 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
             if (lserk) {
               const double rr = first ? pdt_ * r : pa * R[o] + pdt_ * r;
               __stcs(p.res + gofs + o, rr);
-              __stcs(p.u_out + gofs + o, U[o] + pb * rr);
+              __stcs(p.u_out + gofs + o, Us[(f * NQ + j) * SP + i] + pb * rr);
             } else {
               __stcs(p.rhs_out + gofs + o, accum ? R[o] + r : r);
             }
