@@ -25,7 +25,8 @@ __host__ __device__ constexpr int npt_of(int N) { return (N + 1) * (N + 2) * (N 
 __host__ __device__ constexpr int fw_of(int N) { return 2 * nt_of(N) + 3 * nq_of(N) * nq_of(N); }
 /// doubles per wedge geometry record
 __host__ __device__ constexpr int wg_of(int N) { return 44 + 2 * nq_of(N); }
-constexpr int kTG = 36; // doubles per tet record
+constexpr int kTG = 38; // doubles per tet record (36 used; 38 spreads the shared-memory banks of
+                        // the per-tet record reads in the tet DMMA kernel epilogue)
 constexpr int kWC = 12; // ints per wedge connectivity record (5 x {nbr, map} + pad, 48 B)
 __host__ __device__ constexpr int even_up(int x) { return (x + 1) & ~1; }
 __host__ __device__ constexpr int ceil_div(int a, int b) { return (a + b - 1) / b; }

@@ -58,6 +58,13 @@ constexpr int kComboCapT = 2048; // ints of neighbour node maps kept in shared m
 #endif
 __host__ __device__ constexpr bool tet_tables_global(int N) { return N >= PDG_TET_TG_MIN_N; }
 
+#ifndef PDG_TET_PAD_STATE
+#define PDG_TET_PAD_STATE 1
+#endif
+__host__ __device__ constexpr int tet_slot_stride(int x) {
+  return (x % 8 == 2 && x % 2 == 0) ? x : tet_slot_stride(x + 1);
+}
+
 template <int N, int NST_>
 struct TDCfg {
   static constexpr int NP = npt_of(N), NT = nt_of(N);
@@ -74,7 +81,11 @@ struct TDCfg {
   static constexpr int FST = cf_stride(NT);   // flux-buffer column stride
   // per-stage buffers: state, records, connectivity of 8 tets (the residual
   // goes straight from HBM into registers in the epilogue pattern)
-  static constexpr int UB = kTB * 4 * NP;
+  // per-tet state slot stride: 2 US = 4 or 12 mod 16 doubles, so the tets
+  // 2 tig + c read by one warp instruction fall on distinct bank pairs
+  // measured (profiles/round1_pad_state_ab.txt): N = 2, 3 -5%, N = 4, 5 neutral
+  static constexpr int US = (PDG_TET_PAD_STATE && N <= 3) ? tet_slot_stride(4 * NP) : 4 * NP;
+  static constexpr int UB = kTB * US;
   static constexpr int STAGE = r2(UB + kTB * kTG + kTB * 8 / 2);
   static constexpr int TASKS = ceil_div(kTB * 4 * NT, 32 * IT); // face-node tasks per thread
   static constexpr int BV = 4 * kTB * VST;    // [P | W_r | W_s | W_t] x 8 tets
@@ -111,7 +122,12 @@ __device__ __forceinline__ void load_batch(const StageParams& p, double* stg, lo
   const uint32_t bytes = ub + 8u * kTG * nel + 32u * nel;
   const uint64_t keep = l2_policy_evict_last(), stream = l2_policy_evict_first();
   mbar_arrive_expect_tx(bar, bytes);
-  tma_load_1d_hint(U, p.u_in + p.tet_base + t0 * 4 * NP, ub, bar, keep);
+  if (C::US == 4 * NP) {
+    tma_load_1d_hint(U, p.u_in + p.tet_base + t0 * 4 * NP, ub, bar, keep);
+  } else {
+    for (int t = 0; t < nel; ++t) // one bulk copy per tet into its padded slot
+      tma_load_1d_hint(U + t * C::US, p.u_in + p.tet_base + (t0 + t) * 4 * NP, 32u * NP, bar, keep);
+  }
   tma_load_1d_hint(G, p.tgeo + t0 * kTG, 8u * kTG * nel, bar, stream);
   tma_load_1d_hint(G + kTB * kTG, p.tconn + t0 * 8, 32u * nel, bar, stream);
 }
@@ -269,7 +285,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
         if (m < nel * 4 * NT) {
           const int t = m / (4 * NT), fm = m - t * 4 * NT;
           const int f = fm / NT, loc = fm - f * NT;
-          const double* Ut = U + t * 4 * NP;
+          const double* Ut = U + t * C::US;
           const double* Gt = G + t * kTG;
           const int my = sFace[fm];
           const double pm = Ut[my];
@@ -296,7 +312,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
     if (vol) {
       for (int m = tt; m < nel * NP; m += 32 * T) {
         const int t = m / NP, n = m - t * NP;
-        const double* Ut = U + t * 4 * NP;
+        const double* Ut = U + t * C::US;
         const double* Gt = G + t * kTG;
         const double ux = Ut[NP + n], uy = Ut[2 * NP + n], uz = Ut[3 * NP + n];
         BVb[t * VST + n] = Ut[n];
@@ -367,7 +383,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
           ruz *= irho;
         }
         const double rv[4] = {rp, rux, ruy, ruz};
-        const double* Ut = U + t * 4 * NP;
+        const double* Ut = U + t * C::US;
         const long long go = p.tet_base + (t0 + t) * 4 * NP + n;
 #pragma unroll
         for (int fld = 0; fld < 4; ++fld) {
