@@ -18,17 +18,22 @@ template <int N, bool TO_DEVICE>
 __global__ void layout_kernel(long long Kw, long long Kt, const int* __restrict__ dev_to_ref,
                               const long long* __restrict__ ref_offset,
                               const double* __restrict__ src, double* __restrict__ dst) {
-  constexpr int NQ = nq_of(N), NT = nt_of(N), NPW = npw_of(N), NPT = npt_of(N);
-  const long long wdofs = Kw * 4 * NPW;
+  // device wedge block: 4 fields x NQ slices x ST (>= NT, padding entries are zero)
+  constexpr int NQ = nq_of(N), NT = nt_of(N), NPW = npw_of(N), NPD = npd_of(N), ST = nts_of(N), NPT = npt_of(N);
+  const long long wdofs = Kw * 4 * NPD;
   const long long total = wdofs + Kt * 4 * NPT;
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
     long long d, ref_local;
     if (idx < wdofs) {
-      d = idx / (4 * NPW);
-      const int off = (int)(idx - d * 4 * NPW);
-      const int fld = off / NPW, node = off - fld * NPW;
-      const int j = node / NT, i = node - j * NT;
+      d = idx / (4 * NPD);
+      const int off = (int)(idx - d * 4 * NPD);
+      const int fld = off / NPD, node = off - fld * NPD;
+      const int j = node / ST, i = node - j * ST;
+      if (i >= NT) { // slice padding
+        if (TO_DEVICE) dst[idx] = 0.0;
+        continue;
+      }
       ref_local = (long long)fld * NPW + i * NQ + j;
     } else {
       const long long t = (idx - wdofs) / (4 * NPT);
@@ -46,7 +51,8 @@ __global__ void layout_kernel(long long Kw, long long Kt, const int* __restrict_
 template <int N>
 __global__ void wedge_energy_kernel(const EnergyParams p, int elems_per_block) {
   // thread (el, i); partial energy of each block written to partials[block]
-  constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npw_of(N), WG = wg_of(N);
+  // NP = device per-field block, ST = device slice stride
+  constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npd_of(N), ST = nts_of(N), WG = wg_of(N);
   extern __shared__ double smem[];
   const int E = elems_per_block;
   double* sU = smem;                // [E][4*NP]
@@ -70,7 +76,7 @@ __global__ void wedge_energy_kernel(const EnergyParams p, int elems_per_block) {
       for (int k = 0; k < NT; ++k) {
         const double m = j0 * p.Mtri[k * NT + i] + jr * p.Xr[k * NT + i] + js * p.Xs[k * NT + i];
 #pragma unroll
-        for (int l = 0; l < NQ; ++l) vm[l] += v[l * NT + k] * m;
+        for (int l = 0; l < NQ; ++l) vm[l] += v[l * ST + k] * m;
       }
       double q = 0.0;
 #pragma unroll
@@ -83,7 +89,7 @@ __global__ void wedge_energy_kernel(const EnergyParams p, int elems_per_block) {
 #pragma unroll
           for (int l = 0; l < NQ; ++l) mv += p.M1D[j * NQ + l] * vm[l];
         }
-        q += v[j * NT + i] * mv;
+        q += v[j * ST + i] * mv;
       }
       acc += (fld == 0 ? ikap : rho) * q;
     }
@@ -153,7 +159,7 @@ template <int N>
 __global__ void check_finite_kernel(long long Kw, long long Kt, const double* __restrict__ u,
                                     const int* __restrict__ dev_to_ref,
                                     unsigned long long* first_bad) {
-  constexpr int NPW = npw_of(N), NPT = npt_of(N);
+  constexpr int NPW = npd_of(N), NPT = npt_of(N); // device wedge block (padding entries are zero)
   const long long wdofs = Kw * 4 * NPW;
   const long long total = wdofs + Kt * 4 * NPT;
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
@@ -169,18 +175,25 @@ template <int N, bool PACK>
 __global__ void pack_kernel(long long Kw, const long long* __restrict__ elems, long long n,
                             const double* __restrict__ src, double* __restrict__ dst) {
   // one CTA per listed element; wedge and tet blocks have different sizes
-  constexpr int NPW = npw_of(N), NPT = npt_of(N);
+  // buffer entries: 4 x Np per element (device node order, no slice padding);
+  // device state: wedge blocks of 4 x NPD (slices of ST)
+  constexpr int NT = nt_of(N), NPW = npw_of(N), NPD = npd_of(N), ST = nts_of(N), NPT = npt_of(N);
   for (long long q = blockIdx.x; q < n; q += gridDim.x) {
     const long long d = elems[q];
     const bool wedge = d < Kw;
     const int len = 4 * (wedge ? NPW : NPT);
-    const long long off = wedge ? d * 4 * NPW : Kw * 4 * NPW + (d - Kw) * 4 * NPT;
+    const long long off = wedge ? d * 4 * NPD : Kw * 4 * NPD + (d - Kw) * 4 * NPT;
     const long long boff = q * 4 * (NPW > NPT ? NPW : NPT);
     for (int k = threadIdx.x; k < len; k += blockDim.x) {
+      long long o = k;
+      if (wedge && ST != NT) {
+        const int fld = k / NPW, node = k - fld * NPW, j = node / NT, i = node - j * NT;
+        o = (long long)fld * NPD + j * ST + i;
+      }
       if (PACK)
-        dst[boff + k] = src[off + k];
+        dst[boff + k] = src[off + o];
       else
-        dst[off + k] = src[boff + k];
+        dst[off + o] = src[boff + k];
     }
   }
 }
@@ -211,7 +224,7 @@ int grid_for(long long total, int threads) {
 cudaError_t launch_to_device_layout(int N, long long Kw, long long Kt, const int* dev_to_ref,
                                     const long long* ref_offset, const double* src, double* dst,
                                     cudaStream_t s) {
-  const long long total = Kw * 4 * npw_of(N) + Kt * 4 * npt_of(N);
+  const long long total = Kw * 4 * npd_of(N) + Kt * 4 * npt_of(N);
   if (total == 0) return cudaSuccess;
   PDG_DISPATCH(N, (layout_kernel<NN, true><<<grid_for(total, 256), 256, 0, s>>>(Kw, Kt, dev_to_ref, ref_offset, src, dst)));
   return cudaGetLastError();
@@ -220,7 +233,7 @@ cudaError_t launch_to_device_layout(int N, long long Kw, long long Kt, const int
 cudaError_t launch_to_reference_layout(int N, long long Kw, long long Kt, const int* dev_to_ref,
                                        const long long* ref_offset, const double* src, double* dst,
                                        cudaStream_t s) {
-  const long long total = Kw * 4 * npw_of(N) + Kt * 4 * npt_of(N);
+  const long long total = Kw * 4 * npd_of(N) + Kt * 4 * npt_of(N);
   if (total == 0) return cudaSuccess;
   PDG_DISPATCH(N, (layout_kernel<NN, false><<<grid_for(total, 256), 256, 0, s>>>(Kw, Kt, dev_to_ref, ref_offset, src, dst)));
   return cudaGetLastError();
@@ -232,7 +245,7 @@ cudaError_t launch_energy(int N, const EnergyParams& p, int* nblocks_out, cudaSt
   const int E = (256 / NT) > 0 ? 256 / NT : 1;
   if (p.Kw > 0) {
     wb = (int)((p.Kw + E - 1) / E);
-    const size_t smem = ((size_t)E * 4 * npw_of(N) + (size_t)E * NT) * 8;
+    const size_t smem = ((size_t)E * 4 * npd_of(N) + (size_t)E * NT) * 8;
     PDG_DISPATCH(N, ({
       cudaFuncSetAttribute(wedge_energy_kernel<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       wedge_energy_kernel<NN><<<wb, E * NT, smem, s>>>(p, E);
@@ -299,7 +312,7 @@ cudaError_t launch_unpack_states(int N, long long Kw, const long long* dev_elems
 cudaError_t launch_check_finite(int N, long long Kw, long long Kt, const double* u,
                                 const int* dev_to_ref, unsigned long long* first_bad,
                                 cudaStream_t s) {
-  const long long total = Kw * 4 * npw_of(N) + Kt * 4 * npt_of(N);
+  const long long total = Kw * 4 * npd_of(N) + Kt * 4 * npt_of(N);
   if (total == 0) return cudaSuccess;
   PDG_DISPATCH(N, (check_finite_kernel<NN><<<grid_for(total, 256), 256, 0, s>>>(Kw, Kt, u, dev_to_ref, first_bad)));
   return cudaGetLastError();

@@ -128,7 +128,7 @@ void check_device(int device) {
 int dev_node_of(const prismdg::Discretization& d, bool wedge, int nref) {
   if (!wedge) return nref;
   const int i = nref / d.nq, j = nref - i * d.nq;
-  return j * d.nt + i;
+  return j * nts_of(d.degree) + i; // device slice stride (padded at N = 5)
 }
 
 void launch_checked(pdg_ctx* c, const StageParams& p, bool wedge) {
@@ -286,7 +286,8 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags,
     c->Kw = d.mesh.num_wedges();
     c->Kt = d.mesh.num_tets();
     c->total_dofs = (long long)d.total_dofs;
-    c->tet_base = c->Kw * 4 * c->npw;
+    c->tet_base = c->Kw * 4 * npd_of(c->N);
+    c->dev_dofs = c->tet_base + c->Kt * 4 * c->npt;
     c->mass_mode = d.mass_mode;
     const int N = c->N, nq = c->nq, nt = c->nt, npw = c->npw, npt = c->npt;
     const bool native = flags & 1;
@@ -526,12 +527,15 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags,
     }
 
     // ---- state buffers --------------------------------------------------------
-    const std::size_t nd = (std::size_t)c->total_dofs;
+    // device-layout buffers (slice padding stays zero: no kernel writes it) and
+    // the reference-layout staging buffer
+    const std::size_t nd = (std::size_t)c->dev_dofs;
     c->u[0] = dalloc<double>(nd);
     c->u[1] = dalloc<double>(nd);
     c->res = dalloc<double>(nd);
-    c->stage = dalloc<double>(nd);
+    c->stage = dalloc<double>(std::max<std::size_t>((std::size_t)c->total_dofs, nd));
     PDG_CK(cudaMemsetAsync(c->u[0], 0, nd * 8, c->stream));
+    PDG_CK(cudaMemsetAsync(c->u[1], 0, nd * 8, c->stream));
     PDG_CK(cudaMemsetAsync(c->res, 0, nd * 8, c->stream));
     c->scalar = dalloc<double>(1);
     c->badflag = dalloc<unsigned long long>(1);
@@ -600,7 +604,10 @@ void get_state(pdg_ctx* c, double* u, bool on_device) {
 }
 
 static void ensure_rhs(pdg_ctx* c) {
-  if (!c->rhs) c->rhs = dalloc<double>((std::size_t)c->total_dofs);
+  if (!c->rhs) {
+    c->rhs = dalloc<double>((std::size_t)c->dev_dofs);
+    PDG_CK(cudaMemsetAsync(c->rhs, 0, (std::size_t)c->dev_dofs * 8, c->stream));
+  }
 }
 
 void run_phase(pdg_ctx* c, bool wedge, bool volume) {
@@ -680,9 +687,12 @@ void step_ab3(pdg_ctx* c, double dt, int nsteps) {
   PDG_CK(cudaSetDevice(c->device));
   if (c->Kw_act != c->Kw || c->Kt_act != c->Kt)
     throw prismdg::ConfigError("AB3 on a partitioned context is not supported");
-  const std::size_t nd = (std::size_t)c->total_dofs;
+  const std::size_t nd = (std::size_t)c->dev_dofs;
   for (auto& h : c->fh)
-    if (!h) h = dalloc<double>(nd);
+    if (!h) {
+      h = dalloc<double>(nd);
+      PDG_CK(cudaMemsetAsync(h, 0, nd * 8, c->stream)); // slice padding stays zero
+    }
   for (int n = 0; n < nsteps; ++n) {
     if (c->ab3_filled < 2) {
       // record f at the step start into h[2 - filled], then one LSERK step
@@ -739,8 +749,8 @@ long long trace_offsets(pdg_ctx* c, long long n, const long long* elems, const i
     const bool wedge = d.mesh.kind((int)r) == prismdg::ElemKind::wedge;
     if (f < 0 || f >= d.mesh.num_faces((int)r)) throw prismdg::ConfigError("trace face out of range");
     const long long dev = ref_to_dev[r];
-    const long long base = wedge ? dev * 4 * c->npw : c->tet_base + (dev - c->Kw) * 4 * c->npt;
-    const int np = wedge ? c->npw : c->npt;
+    const long long base = wedge ? dev * 4 * npd_of(c->N) : c->tet_base + (dev - c->Kw) * 4 * c->npt;
+    const int np = wedge ? npd_of(c->N) : c->npt;
     const auto& nodes = d.my_nodes((int)r, f);
     for (int fld = 0; fld < 4; ++fld)
       for (int nref : nodes) out[m++] = base + (long long)fld * np + dev_node_of(d, wedge, nref);

@@ -16,6 +16,7 @@ struct pdg_ctx {
   int flags = 0;
   int N = 0, nq = 0, nt = 0, npw = 0, npt = 0, fw = 0;
   long long Kw = 0, Kt = 0, total_dofs = 0, tet_base = 0;
+  long long dev_dofs = 0; // device state size: wedge blocks padded to nts_of(N) per slice
   long long Kw_act = 0, Kt_act = 0; // owned (computed) elements; ghosts follow them
   long long Kw_int = 0, Kt_int = 0; // owned elements without ghost neighbours (they come first)
   prismdg::MassMode mass_mode = prismdg::MassMode::exact;

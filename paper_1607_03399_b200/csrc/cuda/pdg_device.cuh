@@ -23,6 +23,18 @@ __host__ __device__ constexpr int nt_of(int N) { return (N + 1) * (N + 2) / 2; }
 __host__ __device__ constexpr int npw_of(int N) { return nq_of(N) * nt_of(N); }
 __host__ __device__ constexpr int npt_of(int N) { return (N + 1) * (N + 2) * (N + 3) / 6; }
 __host__ __device__ constexpr int fw_of(int N) { return 2 * nt_of(N) + 3 * nq_of(N) * nq_of(N); }
+/// device slice stride of the wedge state ([field][slice j][tri node i]).
+/// PDG_SLICE_PAD_N5 pads N = 5 slices 21 -> 22 doubles so the DMMA state
+/// fragment loads are bank-conflict free; measured slower (+4.8% state bytes
+/// outweigh the conflicts, profiles/round1_pad_state_ab.txt), so off: every
+/// kernel and layout routine honours nts_of / npd_of, the GPU suite passes
+/// either way.
+#ifndef PDG_SLICE_PAD_N5
+#define PDG_SLICE_PAD_N5 0
+#endif
+__host__ __device__ constexpr int nts_of(int N) { return (PDG_SLICE_PAD_N5 && N == 5) ? nt_of(N) + 1 : nt_of(N); }
+/// device per-field block of a wedge: NQ slices of nts_of(N) (== npw_of(N) unless padded)
+__host__ __device__ constexpr int npd_of(int N) { return nq_of(N) * nts_of(N); }
 /// doubles per wedge geometry record
 __host__ __device__ constexpr int wg_of(int N) { return 44 + 2 * nq_of(N); }
 constexpr int kTG = 38; // doubles per tet record (36 used; 38 spreads the shared-memory banks of

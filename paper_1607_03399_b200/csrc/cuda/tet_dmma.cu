@@ -266,8 +266,8 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
             const double* nb;
             int fs;
             if (nbr < p.Kw) {
-              nb = p.u_in + (long long)nbr * 4 * npw_of(N) + qn;
-              fs = npw_of(N);
+              nb = p.u_in + (long long)nbr * 4 * npd_of(N) + qn;
+              fs = npd_of(N);
             } else {
               nb = ubase + (long long)(nbr - p.Kw) * 4 * NP + qn;
               fs = NP;

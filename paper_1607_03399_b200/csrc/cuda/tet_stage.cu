@@ -78,8 +78,8 @@ tet_stage_kernel(const StageParams p) {
         const double* nb;
         int fs;
         if (nbr < p.Kw) {
-          nb = p.u_in + (long long)nbr * 4 * npw_of(N);
-          fs = npw_of(N);
+          nb = p.u_in + (long long)nbr * 4 * npd_of(N);
+          fs = npd_of(N);
         } else {
           nb = ubase + (long long)(nbr - p.Kw) * 4 * NP;
           fs = NP;

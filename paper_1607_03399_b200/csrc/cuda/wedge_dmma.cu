@@ -69,7 +69,8 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 
 template <int N, int NST_>
 struct DCfg {
-  static constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npw_of(N), FW = fw_of(N), WG = wg_of(N);
+  // NP = device per-field block (NQ slices of ST doubles), ST = device slice stride
+  static constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npd_of(N), ST = nts_of(N), FW = fw_of(N), WG = wg_of(N);
   static constexpr int IT = it_of(N), KS = ks_of(N), KT = kt_of(N);
   static constexpr int JT = ceil_div(NQ, 8), NPJ = 8 * JT;   // slice column tiles
   static constexpr int JTL = ceil_div(NQ + 2, 8);            // [P | Fu0 | Fu1] tiles
@@ -90,7 +91,7 @@ struct DCfg {
   // not 4 or 12 mod 16 (row = field*NQ + slice, stride SP)
   // measured: N = 4 3.93 vs 4.22 ms, N = 5 6.55 vs 6.31 ms (profiles/round1_pad_state_ab.txt)
   static constexpr bool PAD = PDG_PAD_STATE && cf_stride(NT) != NT && N == 4;
-  static constexpr int SP = PAD ? cf_stride(NT) : NT;
+  static constexpr int SP = PAD ? cf_stride(NT) : ST;
   static constexpr int UPS = PAD ? r2((4 * NQ + 8 * JT + 4 * KT) * SP + 4 * KS + 8) : 0;
   static constexpr int WORK = VS + 2 * (FTRI + FQ) + ZS + UPS;
   static constexpr int TABLES = r2(2 * IT * KS * 32 + JT * KT * 32 + 2 * NQ + ceil_div(FW, 2) + kComboCap / 2);
@@ -155,7 +156,7 @@ __device__ __forceinline__ void load_element(const StageParams& p, double* stg, 
 template <int N, bool COMBO_SMEM, bool FUSED, int NST>
 __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(const StageParams p) {
   using C = DCfg<N, NST>;
-  constexpr int NQ = C::NQ, NT = C::NT, NP = C::NP, FW = C::FW, WG = C::WG, T = C::T;
+  constexpr int NQ = C::NQ, NT = C::NT, NP = C::NP, ST = C::ST, FW = C::FW, WG = C::WG, T = C::T;
   constexpr int KS = C::KS, JT = C::JT, JTL = C::JTL, KT = C::KT, VST = C::VST, TPB = C::TPB;
   constexpr int QL_ = C::QF_LANE;
   extern __shared__ __align__(16) double smem[];
@@ -311,8 +312,8 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
     // ---- padded state copy (published by the flux barrier) ----------------------
     if (C::PAD)
       for (int q = tt; q < 4 * NP; q += 32 * T) {
-        const int row = q / NT, col = q - row * NT;
-        Upad[row * SP + col] = U[q];
+        const int row = q / ST, col = q - row * ST;
+        if (col < NT) Upad[row * SP + col] = U[q];
       }
     const double* Us = C::PAD ? Upad : U; // state with row stride SP
 
@@ -486,7 +487,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
 #pragma unroll
         for (int a = 0; a < 3; ++a) n_[f][a] = nrm[3 * f + a];
       // per-lane base offset of position (i, j = 2 tig); (jt, c, field) add constants
-      const int lane_off = 2 * tig * NT + i;
+      const int lane_off = 2 * tig * ST + i;
       const double* Ul = Us + 2 * tig * SP + i; // padded rows: (field*NQ + j)*SP + i
       const double* Rl = R + lane_off;
       const long long gofs = e * 4 * NP + lane_off;
@@ -521,11 +522,11 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
               ruz *= irho;
             }
             const double rv[4] = {rp, rux, ruy, ruz};
-            constexpr int cst[2] = {0, NT};
+            constexpr int cst[2] = {0, ST};
             constexpr int csp[2] = {0, SP};
 #pragma unroll
             for (int f = 0; f < 4; ++f) {
-              const int o = f * NP + 8 * jt * NT + cst[c];
+              const int o = f * NP + 8 * jt * ST + cst[c];
               const int ou = (f * NQ + 8 * jt) * SP + csp[c];
               if (lserk) {
                 const double rr = first ? pdt * rv[f] : pa * Rl[o] + pdt * rv[f];

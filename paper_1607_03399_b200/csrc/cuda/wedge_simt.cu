@@ -82,7 +82,8 @@ __host__ __device__ constexpr int slot_stride(int x, int NT) {
 
 template <int N, bool WADG = false>
 struct SCfg {
-  static constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npw_of(N), FW = fw_of(N), WG = wg_of(N);
+  static_assert(nts_of(N) == nt_of(N), "the low-order kernel assumes an unpadded slice stride");
+  static constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npd_of(N), FW = fw_of(N), WG = wg_of(N);
   static constexpr int THREADS = PDG_SIMT_THREADS;
   static constexpr int E = THREADS / NT;      // wedges per chunk
   static constexpr int ACT = E * NT;          // threads with a (wedge, node) pair

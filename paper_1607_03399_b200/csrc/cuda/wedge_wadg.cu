@@ -57,7 +57,8 @@ constexpr int kComboCapW = 2048; // ints of neighbour node maps kept in shared m
 
 template <int N, int NST_, bool TG = false>
 struct WCfg {
-  static constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npw_of(N), FW = fw_of(N), WG = wg_of(N);
+  // NP = device per-field block (NQ slices of ST doubles), ST = device slice stride
+  static constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npd_of(N), ST = nts_of(N), FW = fw_of(N), WG = wg_of(N);
   static constexpr int IT = it_of(N), KS = ks_of(N), KT = kt_of(N);
   static constexpr int NC = wadg_nc(N), KQ = ceil_div(NC, 4);
   static constexpr int JT = ceil_div(NQ, 8);     // slice column tiles
@@ -84,7 +85,7 @@ struct WCfg {
   // padded state copy for bank-conflict-free fragment loads (see wedge_dmma.cu)
   // measured: N = 4 5.05 -> 4.60 ms, N = 5 8.59 -> 8.86 ms (profiles/round1_pad_state_ab.txt)
   static constexpr bool PAD = PDG_WADG_PAD_STATE && cf_stride(NT) != NT && N == 4;
-  static constexpr int SP = PAD ? cf_stride(NT) : NT;
+  static constexpr int SP = PAD ? cf_stride(NT) : ST;
   static constexpr int UPS = PAD ? r2((4 * NQ + 8 * JT + 4 * KT) * SP + 4 * KS + 8) : 0;
   static constexpr int WORK = BS + 2 * (FTRI + FQ) + IJ + UPS;
   static constexpr int SMEM_BUDGET = 225 * 1024;
@@ -304,8 +305,8 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
 
     if (C::PAD)
       for (int q = tt; q < 4 * NP; q += 32 * T) {
-        const int row = q / NT, col = q - row * NT;
-        Upad[row * SP + col] = U[q];
+        const int row = q / C::ST, col = q - row * C::ST;
+        if (col < NT) Upad[row * SP + col] = U[q];
       }
     const double* Us = C::PAD ? Upad : U; // state with row stride SP, published by the flux barrier
 
@@ -537,7 +538,7 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
             const int f = col / NQ, j = col - f * NQ;
             double r = acc[ct][c];
             if (media) r *= f == 0 ? kappa : irho;
-            const int o = f * NP + j * NT + i;
+            const int o = f * NP + j * C::ST + i;
             if (lserk) {
               const double rr = first ? pdt_ * r : pa * R[o] + pdt_ * r;
               __stcs(p.res + gofs + o, rr);
@@ -621,7 +622,7 @@ constexpr int kEnergyWarps = 4;
 
 template <int N>
 __global__ void __launch_bounds__(32 * kEnergyWarps) wadg_energy_kernel(const EnergyParams p) {
-  constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npw_of(N), NC = wadg_nc(N), WG = wg_of(N);
+  constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npd_of(N), ST = nts_of(N), NC = wadg_nc(N), WG = wg_of(N);
   constexpr int PER_WARP = NT * NT + NT * 4 * NQ + NC + 4 * NP;
   extern __shared__ double smem[];
   __shared__ double part[kEnergyWarps];
@@ -655,7 +656,7 @@ __global__ void __launch_bounds__(32 * kEnergyWarps) wadg_energy_kernel(const En
     // Y(:, col) = Mhat x_col, x_col = slice j of field f (device layout [f][j][i])
     for (int idx = lane; idx < NT * 4 * NQ; idx += 32) {
       const int col = idx / NT, a = idx - col * NT;
-      const double* x = X + col * NT; // f*NP + j*NT = col*NT
+      const double* x = X + col * ST; // device layout: f*NP + j*ST = col*ST
       double sacc = 0.0;
       for (int k = 0; k < NT; ++k) sacc += Mh[a * NT + k] * x[k];
       Y[idx] = sacc;
@@ -707,7 +708,7 @@ __global__ void __launch_bounds__(32 * kEnergyWarps) wadg_energy_kernel(const En
 
 template <int N>
 cudaError_t launch_wadg_energy_N(const EnergyParams& p, int* nb, cudaStream_t s) {
-  constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npw_of(N), NC = wadg_nc(N);
+  constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npd_of(N), NC = wadg_nc(N);
   const size_t smem = (size_t)8 * kEnergyWarps * (NT * NT + NT * 4 * NQ + NC + 4 * NP);
   const int blocks = (int)((p.Kw + kEnergyWarps - 1) / kEnergyWarps);
   *nb = blocks;
