@@ -175,6 +175,15 @@ int pdg_stage_bytes(pdg_ctx* ctx, double* wedge_bytes, double* tet_bytes);
 /* number of device elements and the device element -> reference element map */
 int pdg_device_order(pdg_ctx* ctx, int64_t* dev_to_ref);
 
+/* assemble_global (analysis.cpp:12-40): the dense RHS
+ * operator A(i, j) = d rhs_i / d u_j, reference layout, column-major:
+ * A[j * n + i], n = total_dofs.  Capped at 20000 DOFs like the reference
+ * (kDenseDofCap, analysis.hpp:13; PDG_ERR_ANALYSIS above).  Built from
+ * distance-2 element-coloured batches of unit probes on the device (one rhs
+ * evaluation serves every element of a colour), bitwise equal to probing
+ * column by column. */
+int pdg_assemble_operator(pdg_ctx* ctx, double* A);
+
 /* ---------------------------------------------------------------- partitions
  * Multi-GPU domain decomposition (no reference counterpart: SPEC.md:218 lists
  * distributed runs as a non-goal; this is the north star's sharding).  A rank

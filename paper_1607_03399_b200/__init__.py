@@ -10,7 +10,7 @@ has not been built.
 from . import capi
 from .capi import ConfigError, DeviceError, MeshError, NumericalError, PdgError
 from .solver import (Discretization, DeviceContext, HybridMesh, LayerSpec, RunOptions, RunResult,
-                     SolutionState, arnold_wedge_box, build_discretization, compute_energy, compute_rhs,
+                     SolutionState, assemble_global, spectrum, arnold_wedge_box, build_discretization, compute_energy, compute_rhs,
                      estimate_dt, fit_rate, l2_error, layered_mesh, load_mesh, make_family_mesh,
                      make_initial_state, perturb_vertically, run_simulation, spectra_mesh, stack_layers,
                      structured_hybrid_box, structured_surface, structured_wedge_box, unstructured_wedge_box)

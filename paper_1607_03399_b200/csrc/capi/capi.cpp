@@ -515,6 +515,19 @@ int pdg_step_ab3(pdg_ctx* ctx, double dt, int nsteps, double* t_inout) {
   });
 }
 
+int pdg_assemble_operator(pdg_ctx* ctx, double* A) {
+  return guarded([&] {
+    need(ctx, "context");
+    need(A, "output matrix");
+    const std::size_t n = ctx->disc->total_dofs;
+    if (n > 20000)
+      throw AnalysisError("dense operator assembly capped at 20000 DOFs, mesh has " + std::to_string(n));
+    if (ctx->Kw_act != ctx->Kw || ctx->Kt_act != ctx->Kt)
+      throw ConfigError("operator assembly needs an unpartitioned context");
+    pdg::assemble_operator(ctx, A);
+  });
+}
+
 int pdg_energy(pdg_ctx* ctx, double* energy) {
   return guarded([&] {
     need(ctx, "context");

@@ -90,6 +90,9 @@ void stage_lserk(pdg_ctx* c, double dt, int stage, int part = 0);
 /// device-layout state offsets of the face traces (4 fields x face nodes) of
 /// (reference element, face) pairs; returns the number written
 long long trace_offsets(pdg_ctx* c, long long n, const long long* elems, const int* faces, long long* out);
+/// dense RHS operator (assemble_global, analysis.cpp:12-40), column-major n x n
+/// in the reference layout, from distance-2 colored batches of unit probes
+void assemble_operator(pdg_ctx* c, double* A);
 void gather_values(pdg_ctx* c, const long long* idx, long long n, double* buf, cudaStream_t s = nullptr);
 void scatter_values(pdg_ctx* c, const long long* idx, long long n, const double* buf, cudaStream_t s = nullptr);
 void pack_states(pdg_ctx* c, const long long* dev_elems, long long n, double* buf);

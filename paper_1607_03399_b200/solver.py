@@ -445,3 +445,18 @@ def fit_rate(h, err):
     h = np.asarray(h, dtype=float)[-3:]
     e = np.asarray(err, dtype=float)[-3:]
     return float(np.polyfit(np.log(h), np.log(e), 1)[0])
+
+
+def assemble_global(disc: Discretization) -> np.ndarray:
+    """assemble_global (analysis.cpp:12-40): dense RHS operator, n x n (numpy,
+    A[i, j] = d rhs_i / d u_j), built on the GPU from colored unit probes."""
+    n = int(disc.total_dofs)
+    a = np.zeros((n, n), order="F")
+    check(lib().pdg_assemble_operator(disc.device().handle, a.ctypes.data_as(capi.DP)))
+    return a
+
+
+def spectrum(A: np.ndarray) -> np.ndarray:
+    """spectrum (analysis.cpp:42-52): eigenvalues sorted by real then imaginary part."""
+    ev = np.linalg.eigvals(A)
+    return ev[np.lexsort((ev.imag, ev.real))]
