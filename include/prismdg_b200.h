@@ -232,6 +232,16 @@ typedef struct {
   int watchdog_every;
   double blowup_factor;
   int integrator;         /* 0 lserk4, 1 ab3 (dt = estimate * 0.25, solver.hpp:114) */
+  /* snapshots (RunOptions::snapshot_interval / snapshot_cb, solver.cpp:625-644):
+   * at the start and whenever the time passes the next multiple of the
+   * interval the state (reference layout) is streamed device -> pinned host
+   * on a copy stream while stepping continues; snapshot_cb(u, time, index,
+   * user) runs on the calling thread once the copy has landed (at the latest
+   * by the next snapshot or the end of the run).  interval <= 0 or a NULL
+   * callback: no snapshots. */
+  double snapshot_interval;
+  void (*snapshot_cb)(const double* u, double time, int index, void* user);
+  void* snapshot_user;
 } pdg_run_options;
 
 typedef struct {

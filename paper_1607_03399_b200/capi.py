@@ -68,11 +68,15 @@ class DiscInfo(C.Structure):
     ]
 
 
+SNAPSHOT_CB = C.CFUNCTYPE(None, C.POINTER(C.c_double), C.c_double, C.c_int, C.c_void_p)
+
+
 class RunOptions(C.Structure):
     _fields_ = [
         ("final_time", C.c_double), ("cfl", C.c_double), ("fixed_dt", C.c_double),
         ("energy_interval", C.c_double), ("watchdog_every", C.c_int), ("blowup_factor", C.c_double),
-        ("integrator", C.c_int),
+        ("integrator", C.c_int), ("snapshot_interval", C.c_double), ("snapshot_cb", SNAPSHOT_CB),
+        ("snapshot_user", C.c_void_p),
     ]
 
 

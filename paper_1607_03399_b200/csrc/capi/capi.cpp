@@ -611,6 +611,13 @@ int pdg_run_simulation(pdg_ctx* ctx, double* u_inout, double* time_inout, const 
     };
     log_energy(t, res.initial_energy);
     double next_energy_t = t + opts->energy_interval;
+    pdg::SnapshotStream snaps(ctx, opts->snapshot_cb, opts->snapshot_user);
+    const bool snapshots = opts->snapshot_cb && opts->snapshot_interval > 0.0;
+    double next_snapshot_t = t;
+    if (snapshots) {
+      snaps.take(t);
+      next_snapshot_t += opts->snapshot_interval;
+    }
     for (int n = 0; n < steps; ++n) {
       if (ab3)
         pdg::step_ab3(ctx, dt, 1);
@@ -623,6 +630,10 @@ int pdg_run_simulation(pdg_ctx* ctx, double* u_inout, double* time_inout, const 
         log_energy(t, pdg::energy(ctx));
         while (next_energy_t <= t + 1e-12) next_energy_t += opts->energy_interval;
       }
+      if (snapshots && t + 1e-12 >= next_snapshot_t) {
+        snaps.take(t);
+        while (next_snapshot_t <= t + 1e-12) next_snapshot_t += opts->snapshot_interval;
+      }
       if ((n + 1) % opts->watchdog_every == 0 || n + 1 == steps) {
         const long long bad = pdg::check_finite(ctx);
         if (bad >= 0)
@@ -634,6 +645,7 @@ int pdg_run_simulation(pdg_ctx* ctx, double* u_inout, double* time_inout, const 
                                " to " + std::to_string(en) + " at time " + std::to_string(t));
       }
     }
+    snaps.flush();
     res.final_time = t;
     res.final_energy = pdg::energy(ctx);
     res.num_logged = nlog;

@@ -737,6 +737,57 @@ void stage_lserk(pdg_ctx* c, double dt, int s, int part) {
   c->cur = 1 - c->cur;
 }
 
+SnapshotStream::SnapshotStream(pdg_ctx* c, Callback cb, void* user) : c_(c), cb_(cb), user_(user) {}
+
+SnapshotStream::~SnapshotStream() {
+  if (copy_) cudaStreamSynchronize(copy_);
+  for (int k = 0; k < 2; ++k) {
+    if (dev_[k]) cudaFree(dev_[k]);
+    if (host_[k]) cudaFreeHost(host_[k]);
+    if (done_[k]) cudaEventDestroy(done_[k]);
+  }
+  if (copy_) cudaStreamDestroy(copy_);
+}
+
+void SnapshotStream::deliver() {
+  if (!pending_) return;
+  const int k = (count_ - 1) & 1;
+  PDG_CK(cudaEventSynchronize(done_[k]));
+  pending_ = false;
+  cb_(host_[k], pending_time_, count_ - 1, user_);
+}
+
+void SnapshotStream::take(double time) {
+  PDG_CK(cudaSetDevice(c_->device));
+  const std::size_t n = (std::size_t)c_->total_dofs;
+  if (!copy_) {
+    PDG_CK(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; ++k) {
+      dev_[k] = dalloc<double>(n);
+      PDG_CK(cudaMallocHost(&host_[k], std::max<std::size_t>(n, 1) * 8));
+      PDG_CK(cudaEventCreateWithFlags(&done_[k], cudaEventDisableTiming));
+    }
+  }
+  deliver(); // the previous snapshot (other buffer pair) is handed over first
+  const int k = count_ & 1;
+  PDG_CK(launch_to_reference_layout(c_->N, c_->Kw, c_->Kt, c_->dev_to_ref, c_->ref_offset, c_->u[c_->cur], dev_[k],
+                                    c_->stream));
+  cudaEvent_t ready = nullptr;
+  PDG_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  PDG_CK(cudaEventRecord(ready, c_->stream));
+  PDG_CK(cudaStreamWaitEvent(copy_, ready, 0));
+  PDG_CK(cudaMemcpyAsync(host_[k], dev_[k], n * 8, cudaMemcpyDeviceToHost, copy_));
+  PDG_CK(cudaEventRecord(done_[k], copy_));
+  cudaEventDestroy(ready);
+  pending_ = true;
+  pending_time_ = time;
+  ++count_;
+}
+
+void SnapshotStream::flush() {
+  if (copy_) deliver();
+}
+
 void assemble_operator(pdg_ctx* c, double* A) {
   // A(:, j) = rhs(e_j).  A unit probe in element e only reaches the rows of e
   // and its face neighbours, and those rows only read e, its neighbours and

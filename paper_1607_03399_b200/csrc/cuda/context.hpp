@@ -90,6 +90,33 @@ void stage_lserk(pdg_ctx* c, double dt, int stage, int part = 0);
 /// device-layout state offsets of the face traces (4 fields x face nodes) of
 /// (reference element, face) pairs; returns the number written
 long long trace_offsets(pdg_ctx* c, long long n, const long long* elems, const int* faces, long long* out);
+/// Snapshot streaming of the run driver: the current state is converted to
+/// the reference layout into one of two device buffers on the compute stream,
+/// copied to one of two pinned host buffers on a copy stream (overlapping the
+/// following steps), and handed to the callback once landed -- at the latest
+/// when the next snapshot is taken or at flush().
+class SnapshotStream {
+ public:
+  using Callback = void (*)(const double* u, double time, int index, void* user);
+  SnapshotStream(pdg_ctx* c, Callback cb, void* user);
+  ~SnapshotStream();
+  void take(double time);
+  void flush();
+
+ private:
+  void deliver();
+  pdg_ctx* c_;
+  Callback cb_;
+  void* user_;
+  cudaStream_t copy_ = nullptr;
+  double* dev_[2] = {nullptr, nullptr};
+  double* host_[2] = {nullptr, nullptr};
+  cudaEvent_t done_[2] = {nullptr, nullptr};
+  int count_ = 0;
+  bool pending_ = false;
+  double pending_time_ = 0.0;
+};
+
 /// dense RHS operator (assemble_global, analysis.cpp:12-40), column-major n x n
 /// in the reference layout, from distance-2 colored batches of unit probes
 void assemble_operator(pdg_ctx* c, double* A);

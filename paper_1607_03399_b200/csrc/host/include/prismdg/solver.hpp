@@ -82,6 +82,8 @@ struct RunOptions {
   std::ostream* energy_csv = nullptr;
   int watchdog_every = 50;
   double blowup_factor = 10.0;
+  double snapshot_interval = 0.0; // 0: no snapshots (solver.hpp:133-134)
+  std::function<void(const SolutionState&, int)> snapshot_cb;
 };
 
 struct RunResult {

@@ -230,6 +230,23 @@ RunResult run_simulation(const Discretization& d, SolutionState& state, const Ru
   o.watchdog_every = opts.watchdog_every;
   o.blowup_factor = opts.blowup_factor;
   o.integrator = opts.integrator == IntegratorKind::lserk4 ? 0 : 1;
+  // snapshots: the device driver streams the state to host; the trampoline
+  // wraps it in a SolutionState for the reference-style callback
+  struct Tramp {
+    const RunOptions* opts;
+    std::size_t n;
+  } tramp{&opts, d.total_dofs};
+  if (opts.snapshot_cb && opts.snapshot_interval > 0.0) {
+    o.snapshot_interval = opts.snapshot_interval;
+    o.snapshot_cb = [](const double* u, double time, int index, void* user) {
+      const auto* t = static_cast<const Tramp*>(user);
+      SolutionState s;
+      s.u.assign(u, u + t->n);
+      s.time = time;
+      t->opts->snapshot_cb(s, index);
+    };
+    o.snapshot_user = &tramp;
+  }
   pdg_run_result r{};
   const int max_log = 1 << 20;
   std::vector<double> log(2 * (std::size_t)max_log);

@@ -412,6 +412,8 @@ class RunOptions:
     watchdog_every: int = 50
     blowup_factor: float = 10.0
     integrator: str = "lserk4"  # IntegratorKind: "lserk4" | "ab3"
+    snapshot_interval: float = 0.0  # 0: no snapshots
+    snapshot_cb: object = None  # callable(u: np.ndarray (copy), time: float, index: int)
 
 
 @dataclass
@@ -427,8 +429,19 @@ class RunResult:
 
 def run_simulation(disc: Discretization, state: SolutionState, opts: RunOptions, max_log=100000) -> RunResult:
     """run_simulation (solver.hpp:148-149), state resident on the GPU for the run."""
+    n = int(disc.total_dofs)
+    if opts.snapshot_cb is not None and opts.snapshot_interval > 0.0:
+        user_cb = opts.snapshot_cb
+
+        def _cb(u_ptr, t, index, _user):
+            user_cb(np.ctypeslib.as_array(u_ptr, shape=(n,)).copy(), float(t), int(index))
+
+        cb = capi.SNAPSHOT_CB(_cb)
+    else:
+        cb = capi.SNAPSHOT_CB()
     o = capi.RunOptions(opts.final_time, opts.cfl, opts.fixed_dt, opts.energy_interval,
-                        opts.watchdog_every, opts.blowup_factor, 1 if opts.integrator == "ab3" else 0)
+                        opts.watchdog_every, opts.blowup_factor, 1 if opts.integrator == "ab3" else 0,
+                        opts.snapshot_interval, cb, None)
     r = capi.RunResult()
     log = np.zeros(2 * max_log)
     t = C.c_double(state.time)
