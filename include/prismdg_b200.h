@@ -126,6 +126,9 @@ int pdg_disc_l2_error(const pdg_disc* d, const double* u, double time, double* e
  * jf_quad[6],volume,surface_area} (18) */
 int pdg_disc_wedge_ops(const pdg_disc* d, int64_t w, double* tri_lift, double* quad_lift,
                        double* scalars);
+/* write_vtk_snapshot (snapshot.hpp / snapshot.cpp:68-139): legacy ASCII VTK of
+ * the reference-layout state u on the nodal lattice sub-cells */
+int pdg_write_vtk(const pdg_disc* d, const double* u, const char* path);
 void pdg_disc_free(pdg_disc* d);
 
 /* ---------------------------------------------------------------- device path */

@@ -13,7 +13,8 @@ from .solver import (Discretization, DeviceContext, HybridMesh, LayerSpec, RunOp
                      SolutionState, assemble_global, spectrum, arnold_wedge_box, build_discretization, compute_energy, compute_rhs,
                      estimate_dt, fit_rate, l2_error, layered_mesh, load_mesh, make_family_mesh,
                      make_initial_state, perturb_vertically, run_simulation, spectra_mesh, stack_layers,
-                     structured_hybrid_box, structured_surface, structured_wedge_box, unstructured_wedge_box)
+                     structured_hybrid_box, structured_surface, structured_wedge_box, unstructured_wedge_box,
+                     write_vtk_snapshot)
 
 capi.lib()  # load now: no silent fallback
 

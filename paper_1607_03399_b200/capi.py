@@ -154,6 +154,7 @@ SIGNATURES = {
     "pdg_unpack_states": (C.c_int, [P, P, C.c_int64, P]),
     "pdg_partition_counts": (C.c_int, [P, I64P]),
     "pdg_assemble_operator": (C.c_int, [P, DP]),
+    "pdg_write_vtk": (C.c_int, [P, DP, C.c_char_p]),
     "pdg_step_stage_part": (C.c_int, [P, C.c_double, C.c_int, C.c_int]),
     "pdg_trace_offsets": (C.c_int, [P, C.c_int64, I64P, IP, I64P, I64P]),
     "pdg_gather_values": (C.c_int, [P, P, C.c_int64, P, P]),

@@ -2,6 +2,7 @@
 // Opaque handles: pdg_mesh* is a prismdg::HybridMesh*, pdg_disc* a
 // prismdg::Discretization*, pdg_ctx* the device context (cuda/context.hpp).
 #include "prismdg_b200.h"
+#include "prismdg/snapshot.hpp"
 
 #include <algorithm>
 #include <cmath>
@@ -365,6 +366,15 @@ int pdg_disc_wedge_ops(const pdg_disc* dh, int64_t w, double* tri_lift, double* 
                             g.jf_quad[2][0], g.jf_quad[2][1], g.volume, g.surface_area};
       std::copy(v, v + 18, scalars);
     }
+  });
+}
+
+int pdg_write_vtk(const pdg_disc* dh, const double* u, const char* path) {
+  return guarded([&] {
+    need(dh, "discretization");
+    need(u, "state");
+    need(path, "path");
+    write_vtk_snapshot(*D(dh), u, path);
   });
 }
 

@@ -473,3 +473,9 @@ def spectrum(A: np.ndarray) -> np.ndarray:
     """spectrum (analysis.cpp:42-52): eigenvalues sorted by real then imaginary part."""
     ev = np.linalg.eigvals(A)
     return ev[np.lexsort((ev.imag, ev.real))]
+
+
+def write_vtk_snapshot(disc: Discretization, u, path: str) -> None:
+    """write_vtk_snapshot (snapshot.cpp:68-139): legacy ASCII VTK of the nodal state."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    check(lib().pdg_write_vtk(disc.handle, _dp(u), path.encode()))
