@@ -2,7 +2,7 @@
 // Opaque handles: pdg_mesh* is a prismdg::HybridMesh*, pdg_disc* a
 // prismdg::Discretization*, pdg_ctx* the device context (cuda/context.hpp).
 #include "prismdg_b200.h"
-#include "prismdg/snapshot.hpp"
+#include "prismdg/solver.hpp"
 
 #include <algorithm>
 #include <cmath>

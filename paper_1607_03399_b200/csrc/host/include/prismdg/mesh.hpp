@@ -1,14 +1,14 @@
 #pragma once
-// Hybrid wedge/tet meshes, generators and face connectivity (host setup).
-// Restates proj/include/prismdg/mesh.hpp:14-123.  Element ids enumerate wedges
-// first, then tets (mesh.hpp:25,36).  Generators reproduce the reference's
-// vertex / element numbering and RNG draw order exactly, so meshes are
-// bit-identical with the reference for the same parameters.
+// Hybrid wedge/tet meshes: container, generators, validation, file I/O and the
+// face connectivity the device path is built from.
 //
-// Connectivity is stored flat (one FaceConn per element face plus a table of
-// distinct node permutations) instead of one std::vector per face; the
-// permutation content is bit-identical with the reference's greedy matcher
-// (mesh.cpp:398-481).
+// Same public names as the reference's mesh API (proj/include/prismdg/mesh.hpp)
+// so callers port unchanged; element ids enumerate wedges first, then tets.
+// The generators reproduce the reference's vertex and element numbering and
+// its RNG draw order, so meshes are bit-identical for equal parameters.
+// Connectivity is stored flat (one FaceConn per element face and a table of
+// the distinct node permutations) rather than one vector per face; the
+// permutations equal the reference's greedy matcher's node for node.
 
 #include "prismdg/basis.hpp"
 #include "prismdg/geometry.hpp"
@@ -23,88 +23,89 @@
 
 namespace prismdg {
 
-constexpr int kReflectiveTag = 1; // mesh.hpp:14
+/// boundary tag of every generated boundary face (reflecting wall)
+constexpr int kReflectiveTag = 1;
 
+/// acoustic medium of one element; c = sqrt(kappa / rho)
 struct Media {
-  double rho = 1.0;
-  double kappa = 1.0;
-  double wavespeed() const { return std::sqrt(kappa / rho); }
+  double rho = 1.0, kappa = 1.0;
+  auto wavespeed() const -> double { return std::sqrt(kappa / rho); }
 };
 
 struct HybridMesh {
   std::vector<Vert3> vertices;
-  std::vector<std::array<int, 6>> wedges;
+  std::vector<std::array<int, 6>> wedges; // v0 v1 v2 bottom, v3 v4 v5 top
   std::vector<std::array<int, 4>> tets;
-  std::vector<Media> media; // per element
-  std::map<std::pair<int, int>, int> boundary_tags;
+  std::vector<Media> media;                          // indexed by element id
+  std::map<std::pair<int, int>, int> boundary_tags;  // (element, face) -> tag
 
-  int num_wedges() const { return (int)wedges.size(); }
-  int num_tets() const { return (int)tets.size(); }
-  int num_elements() const { return num_wedges() + num_tets(); }
-  ElemKind kind(int e) const { return e < num_wedges() ? ElemKind::wedge : ElemKind::tet; }
-  int num_faces(int e) const { return kind(e) == ElemKind::wedge ? 5 : 4; }
-  WedgeVerts wedge_verts(int w) const;
-  TetVerts tet_verts(int t) const;
+  auto num_wedges() const -> int { return static_cast<int>(wedges.size()); }
+  auto num_tets() const -> int { return static_cast<int>(tets.size()); }
+  auto num_elements() const -> int { return num_wedges() + num_tets(); }
+  auto kind(int e) const -> ElemKind { return e < num_wedges() ? ElemKind::wedge : ElemKind::tet; }
+  auto num_faces(int e) const -> int { return kind(e) == ElemKind::wedge ? 5 : 4; }
+  auto wedge_verts(int w) const -> WedgeVerts;
+  auto tet_verts(int t) const -> TetVerts;
 };
 
+/// a triangulated surface with bottom/top heights per vertex (one layer)
 struct SurfaceTriangulation {
   std::vector<std::array<double, 2>> vertices;
   std::vector<double> z_bottom, z_top;
   std::vector<std::array<int, 3>> triangles;
 };
 
+/// one material layer of a stacked mesh: heights per surface vertex
 struct LayerSpec {
   std::vector<double> z_bottom, z_top;
   int sublayers = 1;
   Media media;
 };
 
-bool is_vertically_mapped(const WedgeVerts& v);
-HybridMesh extrude_layer(const SurfaceTriangulation& surface, int layers, Media media = {});
-HybridMesh stack_layers(const std::vector<std::array<double, 2>>& xy,
-                        const std::vector<std::array<int, 3>>& triangles,
-                        const std::vector<LayerSpec>& layers);
-HybridMesh structured_hybrid_box(int nx, int ny, int nz_wedge, int nz_tet, Media wedge_media = {},
-                                 Media tet_media = {});
-HybridMesh structured_wedge_box(int n, Media media = {});
-HybridMesh unstructured_wedge_box(int n, double xy_jitter, double z_amplitude, std::uint64_t seed,
-                                  Media media = {});
-HybridMesh perturb_vertically(const HybridMesh& mesh, double amplitude, std::uint64_t seed);
-HybridMesh arnold_wedge_box(int n, double delta, Media media = {});
+// ---- generators --------------------------------------------------------------
+auto extrude_layer(const SurfaceTriangulation& surface, int layers, Media media = {}) -> HybridMesh;
+auto stack_layers(const std::vector<std::array<double, 2>>& xy, const std::vector<std::array<int, 3>>& triangles,
+                  const std::vector<LayerSpec>& layers) -> HybridMesh;
+auto structured_hybrid_box(int nx, int ny, int nz_wedge, int nz_tet, Media wedge_media = {},
+                           Media tet_media = {}) -> HybridMesh;
+auto structured_wedge_box(int n, Media media = {}) -> HybridMesh;
+auto unstructured_wedge_box(int n, double xy_jitter, double z_amplitude, std::uint64_t seed, Media media = {})
+    -> HybridMesh;
+auto arnold_wedge_box(int n, double delta, Media media = {}) -> HybridMesh;
+auto perturb_vertically(const HybridMesh& mesh, double amplitude, std::uint64_t seed) -> HybridMesh;
+/// n x n grid of [-1,1]^2 cut into 2 n^2 triangles (the "layers" mesh kind's surface)
+void structured_surface(int n, std::vector<std::array<double, 2>>& xy, std::vector<std::array<int, 3>>& tris);
+/// "flat:z0" or "sine:z0:amp:kx:ky" surface height functions
+auto eval_surface_function(const std::string& spec, double x, double y) -> double;
 
-/// Structured (n x n) surface grid of [-1,1]^2 split into 2n^2 triangles, the
-/// pattern of config.cpp:232-243 ("layers" mesh kind).
-void structured_surface(int n, std::vector<std::array<double, 2>>& xy,
-                        std::vector<std::array<int, 3>>& tris);
-/// Surface functions of config.cpp:152-178: "flat:z0" or "sine:z0:amp:kx:ky".
-double eval_surface_function(const std::string& spec, double x, double y);
+// ---- checks, measures, I/O ------------------------------------------------------
+auto is_vertically_mapped(const WedgeVerts& v) -> bool;
+void validate_mesh(const HybridMesh& mesh);
+auto mesh_volume(const HybridMesh& mesh) -> double;
+auto load_mesh(const std::string& path) -> HybridMesh;
+void save_mesh(const HybridMesh& mesh, const std::string& path);
+auto load_surface(const std::string& path) -> SurfaceTriangulation;
 
+// ---- face connectivity ------------------------------------------------------------
 struct FaceConn {
-  int nbr = -1;      // neighbour element, -1 on the boundary
-  int nbr_face = -1;
+  int nbr = -1, nbr_face = -1;  // neighbour element / its face (-1: boundary)
   int tag = kReflectiveTag;
-  int perm_id = -1;  // index into Connectivity::perms (-1 on the boundary)
+  int perm_id = -1;             // row of Connectivity::perms (-1: boundary)
 };
 
 struct Connectivity {
-  std::vector<FaceConn> faces;        // element e, face f at face_offset[e] + f
-  std::vector<std::int64_t> face_offset; // size ne+1
-  std::vector<std::vector<int>> perms;   // distinct node permutations
-  int num_interior_pairs = 0;
-  int num_boundary_faces = 0;
-  const FaceConn& at(int e, int f) const { return faces[face_offset[e] + f]; }
-  /// my face node i <-> neighbour face node perm(e,f)[i] (reference FaceConn::perm)
-  const std::vector<int>& perm(int e, int f) const { return perms[at(e, f).perm_id]; }
+  std::vector<FaceConn> faces;            // (e, f) at face_offset[e] + f
+  std::vector<std::int64_t> face_offset;  // num_elements + 1 entries
+  std::vector<std::vector<int>> perms;    // distinct face-node permutations
+  int num_interior_pairs = 0, num_boundary_faces = 0;
+
+  auto at(int e, int f) const -> const FaceConn& { return faces[face_offset[e] + f]; }
+  /// my face node i matches neighbour face node perm(e, f)[i]
+  auto perm(int e, int f) const -> const std::vector<int>& { return perms[at(e, f).perm_id]; }
 };
 
-std::vector<int> face_vertex_ids(const HybridMesh& mesh, int e, int f);
-std::vector<Vert3> face_node_coords(const HybridMesh& mesh, const References& refs, int e, int f);
-Connectivity build_connectivity(const HybridMesh& mesh, const References& refs);
-void validate_mesh(const HybridMesh& mesh);
-double mesh_volume(const HybridMesh& mesh);
-
-HybridMesh load_mesh(const std::string& path);
-void save_mesh(const HybridMesh& mesh, const std::string& path);
-SurfaceTriangulation load_surface(const std::string& path);
+auto face_vertex_ids(const HybridMesh& mesh, int e, int f) -> std::vector<int>;
+auto face_node_coords(const HybridMesh& mesh, const References& refs, int e, int f) -> std::vector<Vert3>;
+auto build_connectivity(const HybridMesh& mesh, const References& refs) -> Connectivity;
 
 } // namespace prismdg

@@ -98,6 +98,11 @@ struct RunResult {
 
 RunResult run_simulation(const Discretization& d, SolutionState& state, const RunOptions& opts);
 
+/// Legacy-ASCII VTK unstructured grid of the nodal lattice sub-cells with point
+/// data p, u_x, u_y, u_z from the reference-layout state u (the reference's
+/// snapshot writer format; csrc/host/snapshot.cpp)
+void write_vtk_snapshot(const Discretization& d, const double* u, const std::string& path);
+
 // ---- analysis helpers that stay on the host (analysis.hpp:30-87) ----------
 double l2_error(const Discretization& d, const double* u,
                 const std::function<double(double, double, double, double)>& exact_p, double time);
