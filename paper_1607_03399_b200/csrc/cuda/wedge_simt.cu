@@ -72,6 +72,11 @@ __host__ __device__ constexpr int slot_stride(int x, int NT) {
 #ifndef PDG_SIMT_LATE_OPS
 #define PDG_SIMT_LATE_OPS 1
 #endif
+// rows i of the three quad-face lifts loaded with L and the residual (before
+// the V / gradient phase) instead of at their point of use
+#ifndef PDG_SIMT_QL_EARLY
+#define PDG_SIMT_QL_EARLY 1
+#endif
 #ifndef PDG_SIMT_MINB
 #ifdef PDG_SIMT_MINB_ALL
 #define PDG_SIMT_MINB(N) (PDG_SIMT_MINB_ALL)
@@ -233,12 +238,18 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB(N)) wedg
 
     // per-thread operands from HBM: row i of L, rows i of the quad lifts, residual
     double Lr[NT], rres[4][NQ];
+    double Qr[PDG_SIMT_QL_EARLY && !WADG ? 3 * NQ : 1];
     auto load_operands = [&]() {
       if (active) {
         if (!WADG) {
           const double* L = p.Lt + ge * lcomp_of(N) + i;
 #pragma unroll
           for (int k = 0; k < NT; ++k) Lr[k] = __ldcs(L + k * NT);
+          if (PDG_SIMT_QL_EARLY && surf) {
+            const double* QL = p.QL + ge * qcomp_of(N) + i;
+#pragma unroll
+            for (int fa = 0; fa < 3 * NQ; ++fa) Qr[fa] = __ldcs(QL + fa * NT);
+          }
         }
 #pragma unroll
         for (int f = 0; f < 4; ++f)
@@ -390,7 +401,8 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB(N)) wedg
           for (int j = 0; j < NQ; ++j) qu[j] = 0.0;
 #pragma unroll
           for (int a = 0; a < NQ; ++a) {
-            const double q = __ldcs(QL + (f * NQ + a) * NT);
+            const double q = PDG_SIMT_QL_EARLY ? Qr[(f * NQ + a) % (PDG_SIMT_QL_EARLY ? 3 * NQ : 1)]
+                                               : __ldcs(QL + (f * NQ + a) * NT);
 #pragma unroll
             for (int j = 0; j < NQ; ++j) {
               rp[j] += q * Fe[4 * NT + (f * NQ + a) * NQ + j];
