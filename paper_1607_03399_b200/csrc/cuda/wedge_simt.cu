@@ -37,14 +37,15 @@ namespace {
 
 __host__ __device__ constexpr int r2(int x) { return (x + 1) & ~1; }
 
-/// wavefronts a warp needs to read doubles at addresses {e*S + i}, lane = e*NT + i
-/// (16 eight-byte bank pairs, distinct addresses on one pair serialise)
-__host__ __device__ constexpr int conflict_degree(int S, int NT) {
+/// wavefronts a warp needs to read doubles at addresses {e*S + i}, lane = H (e*NT + i) + h
+/// (16 eight-byte bank pairs, distinct addresses on one pair serialise; the H
+/// lanes of one (e, i) read the same address)
+__host__ __device__ constexpr int conflict_degree(int S, int NT, int H) {
   int worst = 0;
   for (int b = 0; b < 16; ++b) {
     int cnt = 0;
-    for (int lane = 0; lane < 32; ++lane) {
-      const int e = lane / NT, i = lane - e * NT;
+    for (int pr = 0; pr < 32 / H; ++pr) {
+      const int e = pr / NT, i = pr - e * NT;
       if (((e * S + i) & 15) == b) ++cnt;
     }
     worst = cnt > worst ? cnt : worst;
@@ -52,10 +53,10 @@ __host__ __device__ constexpr int conflict_degree(int S, int NT) {
   return worst;
 }
 /// smallest even stride >= x with the least bank conflicts for the {e*S + i} pattern
-__host__ __device__ constexpr int slot_stride(int x, int NT) {
-  int best = r2(x), bd = conflict_degree(r2(x), NT);
+__host__ __device__ constexpr int slot_stride(int x, int NT, int H) {
+  int best = r2(x), bd = conflict_degree(r2(x), NT, H);
   for (int s = r2(x) + 2; s < r2(x) + 16; s += 2) {
-    const int d = conflict_degree(s, NT);
+    const int d = conflict_degree(s, NT, H);
     if (d < bd) {
       bd = d;
       best = s;
@@ -67,8 +68,8 @@ __host__ __device__ constexpr int slot_stride(int x, int NT) {
 #ifndef PDG_SIMT_THREADS
 #define PDG_SIMT_THREADS 128
 #endif
-// minimum resident CTAs per SM (register budget): 3 at N = 1 (measured faster),
-// 1 above (spills), profiles/round1_simt_variants_ab.txt
+// minimum resident CTAs per SM (register budget): 4 at N = 1 with the slice
+// split (3 without), 1 above (spills), profiles/round1_simt_variants_ab.txt
 #ifndef PDG_SIMT_LATE_OPS
 #define PDG_SIMT_LATE_OPS 1
 #endif
@@ -77,11 +78,20 @@ __host__ __device__ constexpr int slot_stride(int x, int NT) {
 #ifndef PDG_SIMT_QL_EARLY
 #define PDG_SIMT_QL_EARLY 1
 #endif
+// threads per (wedge, triangle node) in exact mode: 2 halves the per-thread
+// slice arrays (registers) and the chunk, so more CTAs are resident.  Measured
+// faster at N = 1 only (-6%; +18% at N = 2, 3), profiles/round1_simt_variants_ab.txt
+#ifndef PDG_SIMT_SPLIT
+#define PDG_SIMT_SPLIT(N) ((N) == 1 ? 2 : 1)
+#endif
 #ifndef PDG_SIMT_MINB
 #ifdef PDG_SIMT_MINB_ALL
 #define PDG_SIMT_MINB(N) (PDG_SIMT_MINB_ALL)
 #else
-#define PDG_SIMT_MINB(N) ((N) == 1 ? 3 : 1)
+#ifndef PDG_SIMT_MINB_N1
+#define PDG_SIMT_MINB_N1 (PDG_SIMT_SPLIT(1) > 1 ? 4 : 3)
+#endif
+#define PDG_SIMT_MINB(N) ((N) == 1 ? PDG_SIMT_MINB_N1 : (PDG_SIMT_SPLIT(N) > 1 ? 3 : 1))
 #endif
 #endif
 
@@ -90,17 +100,20 @@ struct SCfg {
   static_assert(nts_of(N) == nt_of(N), "the low-order kernel assumes an unpadded slice stride");
   static constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npd_of(N), FW = fw_of(N), WG = wg_of(N);
   static constexpr int THREADS = PDG_SIMT_THREADS;
-  static constexpr int E = THREADS / NT;      // wedges per chunk
-  static constexpr int ACT = E * NT;          // threads with a (wedge, node) pair
-  static constexpr int SU = slot_stride(4 * NP, NT);
-  static constexpr int SG = slot_stride(WG + kWC / 2, NT); // record + connectivity
+  // H threads per (wedge, node); thread h owns slices j = h, h + H, ... (exact mode)
+  static constexpr int H = WADG ? 1 : PDG_SIMT_SPLIT(N);
+  static constexpr int JH = (NQ + H - 1) / H; // slices per thread
+  static constexpr int E = THREADS / (H * NT); // wedges per chunk
+  static constexpr int ACT = E * NT * H;       // threads with a (wedge, node) pair
+  static constexpr int SU = slot_stride(4 * NP, NT, H);
+  static constexpr int SG = slot_stride(WG + kWC / 2, NT, H); // record + connectivity
   static constexpr int STAGE = E * (SU + SG);
   static constexpr int FT = 4 * NT;                   // tri fluxes: [p|u][bottom|top][NT]
   static constexpr int FQ = 6 * NQ * NQ;              // quad fluxes: [p|u][face][a][j]
-  static constexpr int SF = slot_stride(FT + FQ, NT);
+  static constexpr int SF = slot_stride(FT + FQ, NT, H);
   // exact: V(j, i) at j*NT + i; WADG: the pre-lift buffer B(field, j, i) + 1/J at the cubature
   static constexpr int NC = wadg_nc(N);
-  static constexpr int SV = WADG ? slot_stride(4 * NQ * NT + NC, NT) : slot_stride(NQ * NT, NT);
+  static constexpr int SV = WADG ? slot_stride(4 * NQ * NT + NC, NT, H) : slot_stride(NQ * NT, NT, H);
   // exact: Dr^T, Ds^T; WADG adds kd_m^T [m][k][i], Pw^T [q][i], Vq [q][k], R [m][f][a][i], qr, qs
   static constexpr int WTAB = WADG ? 6 * NT * NT + 2 * NC * NT + 6 * NQ * NT + 2 * NC : 0;
   static constexpr int TABLES = r2(r2(2 * NT * NT + NQ * NQ + 2 * NQ + WTAB) + ceil_div(FW, 2) + 2048 / 2);
@@ -215,7 +228,9 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB(N)) wedg
   if (c < nchunk) load_chunk<N, WADG>(p, stg, p.Kw_begin + c * E, nel_of(c));
   cp_async_commit();
 
-  const int el = threadIdx.x / NT, i = threadIdx.x - el * NT; // this thread's (wedge, node)
+  constexpr int H = C::H, JH = C::JH;
+  const int pr = threadIdx.x / H, h = threadIdx.x - pr * H;
+  const int el = pr / NT, i = pr - el * NT; // this thread's (wedge, node); slices h + H jj
   for (int it = 0; c < nchunk; ++it) {
     double* cur = stg + (it & 1) * C::STAGE;
     // prefetch the next chunk into the other stage (it was released by the
@@ -237,7 +252,7 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB(N)) wedg
     const long long ge = e0 + el;
 
     // per-thread operands from HBM: row i of L, rows i of the quad lifts, residual
-    double Lr[NT], rres[4][NQ];
+    double Lr[NT], rres[4][JH];
     double Qr[PDG_SIMT_QL_EARLY && !WADG ? 3 * NQ : 1];
     auto load_operands = [&]() {
       if (active) {
@@ -254,8 +269,10 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB(N)) wedg
 #pragma unroll
         for (int f = 0; f < 4; ++f)
 #pragma unroll
-          for (int j = 0; j < NQ; ++j)
-            rres[f][j] = res_src ? __ldcs(res_src + ge * 4 * NP + f * NP + j * NT + i) : 0.0;
+          for (int jj = 0; jj < JH; ++jj) {
+            const int j = h + H * jj;
+            rres[f][jj] = res_src && j < NQ ? __ldcs(res_src + ge * 4 * NP + f * NP + j * NT + i) : 0.0;
+          }
       }
     };
     // per-thread operands from HBM (row i of L, residual): issued before the
@@ -339,11 +356,11 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB(N)) wedg
       }
     __syncthreads();
     if constexpr (!WADG) {
-    // ---- V column i, gradients, L products, quad lifts -------------------------------
-    double rp[NQ], rux[NQ], ruy[NQ], ruz[NQ], lp[NQ];
+    // ---- V column i, gradients, L products, quad lifts (own slices j = h + H jj) -------
+    double rp[JH], rux[JH], ruy[JH], ruz[JH], lp[JH];
     double lf0 = 0.0, lf1 = 0.0;
 #pragma unroll
-    for (int j = 0; j < NQ; ++j) rp[j] = rux[j] = ruy[j] = ruz[j] = lp[j] = 0.0;
+    for (int jj = 0; jj < JH; ++jj) rp[jj] = rux[jj] = ruy[jj] = ruz[jj] = lp[jj] = 0.0;
     if (active) {
       const double* Fe = sF + el * SF;
       const double tzJ = G[W_TZJ], jfb = G[W_JFB], jft = G[W_JFT];
@@ -351,19 +368,22 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB(N)) wedg
         const double fb = surf ? jfb * Fe[i] : 0.0, ftop = surf ? jft * Fe[NT + i] : 0.0;
         double* Ve = sV + el * SV;
 #pragma unroll
-        for (int j = 0; j < NQ; ++j) {
-          double d = 0.0;
-          if (vol) {
-            const double sx_ = G[W_TXJ + j], sy_ = G[w_tyj(N) + j];
+        for (int jj = 0; jj < JH; ++jj) {
+          const int j = h + H * jj;
+          if (j < NQ) {
+            double d = 0.0;
+            if (vol) {
+              const double sx_ = G[W_TXJ + j], sy_ = G[w_tyj(N) + j];
 #pragma unroll
-            for (int l = 0; l < NQ; ++l) {
-              const double dt = sDt[j * NQ + l];
-              d += U[NP + l * NT + i] * (sx_ * dt);
-              d += U[2 * NP + l * NT + i] * (sy_ * dt);
-              d += U[3 * NP + l * NT + i] * (tzJ * dt);
+              for (int l = 0; l < NQ; ++l) {
+                const double dt = sDt[j * NQ + l];
+                d += U[NP + l * NT + i] * (sx_ * dt);
+                d += U[2 * NP + l * NT + i] * (sy_ * dt);
+                d += U[3 * NP + l * NT + i] * (tzJ * dt);
+              }
             }
+            Ve[j * NT + i] = -d + fb * sProf[j] + ftop * sProf[NQ + j];
           }
-          Ve[j * NT + i] = -d + fb * sProf[j] + ftop * sProf[NQ + j];
         }
       }
       const double rx = G[W_RX], ry = G[W_RY], sxm = G[W_SX], sym = G[W_SY];
@@ -377,13 +397,16 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB(N)) wedg
           cy = ry * dr + sym * ds;
         }
 #pragma unroll
-        for (int j = 0; j < NQ; ++j) {
-          const double pk = U[j * NT + k];
-          lp[j] += lk * pk;
-          if (vol) {
-            rux[j] -= cx * pk;
-            ruy[j] -= cy * pk;
-            rp[j] -= cx * U[NP + j * NT + k] + cy * U[2 * NP + j * NT + k];
+        for (int jj = 0; jj < JH; ++jj) {
+          const int j = h + H * jj;
+          if (j < NQ) {
+            const double pk = U[j * NT + k];
+            lp[jj] += lk * pk;
+            if (vol) {
+              rux[jj] -= cx * pk;
+              ruy[jj] -= cy * pk;
+              rp[jj] -= cx * U[NP + j * NT + k] + cy * U[2 * NP + j * NT + k];
+            }
           }
         }
         if (surf) {
@@ -396,30 +419,42 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB(N)) wedg
         const double* nrm = G + w_nrm(N);
 #pragma unroll
         for (int f = 0; f < 3; ++f) {
-          double qu[NQ];
+          double qu[JH];
 #pragma unroll
-          for (int j = 0; j < NQ; ++j) qu[j] = 0.0;
+          for (int jj = 0; jj < JH; ++jj) qu[jj] = 0.0;
 #pragma unroll
           for (int a = 0; a < NQ; ++a) {
             const double q = PDG_SIMT_QL_EARLY ? Qr[(f * NQ + a) % (PDG_SIMT_QL_EARLY ? 3 * NQ : 1)]
                                                : __ldcs(QL + (f * NQ + a) * NT);
 #pragma unroll
-            for (int j = 0; j < NQ; ++j) {
-              rp[j] += q * Fe[4 * NT + (f * NQ + a) * NQ + j];
-              qu[j] += q * Fe[4 * NT + 3 * NQ * NQ + (f * NQ + a) * NQ + j];
+            for (int jj = 0; jj < JH; ++jj) {
+              const int j = h + H * jj;
+              if (j < NQ) {
+                rp[jj] += q * Fe[4 * NT + (f * NQ + a) * NQ + j];
+                qu[jj] += q * Fe[4 * NT + 3 * NQ * NQ + (f * NQ + a) * NQ + j];
+              }
             }
           }
           const double nx = nrm[3 * (f + 2)], ny = nrm[3 * (f + 2) + 1], nz = nrm[3 * (f + 2) + 2];
 #pragma unroll
-          for (int j = 0; j < NQ; ++j) {
-            rux[j] += nx * qu[j];
-            ruy[j] += ny * qu[j];
-            ruz[j] += nz * qu[j];
+          for (int jj = 0; jj < JH; ++jj) {
+            rux[jj] += nx * qu[jj];
+            ruy[jj] += ny * qu[jj];
+            ruz[jj] += nz * qu[jj];
           }
         }
       }
     }
     __syncthreads(); // V complete
+    // the whole column LP(:, i) for LY: the other slices come from the partner lanes
+    double lpa[NQ];
+#pragma unroll
+    for (int l = 0; l < NQ; ++l) {
+      const int hh = l % H, jj = l / H;
+      double v = lp[jj];
+      if (H > 1) v = __shfl_sync(0xffffffffu, v, (threadIdx.x & 31) - h + hh);
+      lpa[l] = v;
+    }
 
     // ---- L V, L Y, tri-face velocity lifts, media, LSERK -----------------------------
     if (active) {
@@ -429,43 +464,48 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB(N)) wedg
       for (int k = 0; k < NT; ++k) {
         const double lk = Lr[k];
 #pragma unroll
-        for (int j = 0; j < NQ; ++j) rp[j] += lk * Ve[j * NT + k];
+        for (int jj = 0; jj < JH; ++jj) {
+          const int j = h + H * jj;
+          if (j < NQ) rp[jj] += lk * Ve[j * NT + k];
+        }
       }
       const double* nrm = G + w_nrm(N);
       const double kappa = G[W_KAPPA], irho = G[W_IRHO];
 #pragma unroll
-      for (int j = 0; j < NQ; ++j) {
+      for (int jj = 0; jj < JH; ++jj) {
+        const int j = h + H * jj;
+        if (j >= NQ) continue;
         if (vol) {
           double ly = 0.0;
 #pragma unroll
-          for (int l = 0; l < NQ; ++l) ly += lp[l] * sDt[j * NQ + l];
-          rux[j] -= G[W_TXJ + j] * ly;
-          ruy[j] -= G[w_tyj(N) + j] * ly;
-          ruz[j] -= tzJ * ly;
+          for (int l = 0; l < NQ; ++l) ly += lpa[l] * sDt[j * NQ + l];
+          rux[jj] -= G[W_TXJ + j] * ly;
+          ruy[jj] -= G[w_tyj(N) + j] * ly;
+          ruz[jj] -= tzJ * ly;
         }
         if (surf) {
           const double t0 = jfb * sProf[j] * lf0, t1 = jft * sProf[NQ + j] * lf1;
-          rux[j] += nrm[0] * t0 + nrm[3] * t1;
-          ruy[j] += nrm[1] * t0 + nrm[4] * t1;
-          ruz[j] += nrm[2] * t0 + nrm[5] * t1;
+          rux[jj] += nrm[0] * t0 + nrm[3] * t1;
+          ruy[jj] += nrm[1] * t0 + nrm[4] * t1;
+          ruz[jj] += nrm[2] * t0 + nrm[5] * t1;
         }
         if (media) {
-          rp[j] *= kappa;
-          rux[j] *= irho;
-          ruy[j] *= irho;
-          ruz[j] *= irho;
+          rp[jj] *= kappa;
+          rux[jj] *= irho;
+          ruy[jj] *= irho;
+          ruz[jj] *= irho;
         }
-        const double rv[4] = {rp[j], rux[j], ruy[j], ruz[j]};
+        const double rv[4] = {rp[jj], rux[jj], ruy[jj], ruz[jj]};
 #pragma unroll
         for (int f = 0; f < 4; ++f) {
           const int o = f * NP + j * NT + i;
           const long long go = ge * 4 * NP + o;
           if (lserk) {
-            const double rr = first ? p.dt * rv[f] : p.a * rres[f][j] + p.dt * rv[f];
+            const double rr = first ? p.dt * rv[f] : p.a * rres[f][jj] + p.dt * rv[f];
             __stcs(p.res + go, rr);
             __stcs(p.u_out + go, U[o] + p.b * rr);
           } else {
-            __stcs(p.rhs_out + go, accum ? rres[f][j] + rv[f] : rv[f]);
+            __stcs(p.rhs_out + go, accum ? rres[f][jj] + rv[f] : rv[f]);
           }
         }
       }
