@@ -492,6 +492,84 @@ TEST(hybrid_conformity_acceptance8) {
   CHECK(jump <= 1e-12);
 }
 
+// ---------------------------------------------------------------- mesh files (test_mesh.cpp:277-340)
+static std::string tmp_file(const char* name) {
+  const char* d = std::getenv("TMPDIR");
+  return std::string(d && *d ? d : "/tmp") + "/" + name;
+}
+static void write_text(const std::string& path, const char* text) {
+  std::FILE* f = std::fopen(path.c_str(), "w");
+  std::fputs(text, f);
+  std::fclose(f);
+}
+
+TEST(mesh_file_round_trip) {
+  // perturbed hybrid mesh with media jumps and a boundary tag: every double survives the
+  // 17-digit text form, and the reloaded mesh discretises to the same connectivity
+  HybridMesh mesh = perturb_vertically(structured_hybrid_box(2, 2, 1, 1, {1.0, 1.0}, {1.5, 3.0}), 0.2, 7);
+  mesh.boundary_tags[{0, 0}] = 3;
+  const std::string path = tmp_file("pdg_roundtrip.mesh");
+  save_mesh(mesh, path);
+  const HybridMesh loaded = load_mesh(path);
+  CHECK(loaded.vertices == mesh.vertices);
+  CHECK(loaded.wedges == mesh.wedges);
+  CHECK(loaded.tets == mesh.tets);
+  CHECK(loaded.media.size() == mesh.media.size());
+  for (std::size_t e = 0; e < mesh.media.size(); ++e)
+    CHECK(loaded.media[e].rho == mesh.media[e].rho && loaded.media[e].kappa == mesh.media[e].kappa);
+  CHECK(loaded.boundary_tags == mesh.boundary_tags);
+  const Discretization a = build_discretization(mesh, 2), b = build_discretization(loaded, 2);
+  bool same = a.total_dofs == b.total_dofs;
+  for (int e = 0; same && e < a.num_elements(); ++e)
+    for (int f = 0; f < a.mesh.num_faces(e); ++f)
+      same = same && a.conn.at(e, f).nbr == b.conn.at(e, f).nbr && a.conn.at(e, f).nbr_face == b.conn.at(e, f).nbr_face &&
+             a.conn.at(e, f).tag == b.conn.at(e, f).tag &&
+             (a.conn.at(e, f).nbr < 0 || a.conn.perm(e, f) == b.conn.perm(e, f));
+  CHECK(same);
+  std::remove(path.c_str());
+}
+
+TEST(mesh_loader_rejects_invalid) {
+  const std::string path = tmp_file("pdg_bad.mesh");
+  // top vertex shifted in x: not vertically mapped, error names the wedge
+  write_text(path, "$Vertices\n6\n0 0 0\n1 0 0\n0 1 0\n0.5 0 1\n1 0 1\n0 1 1\n$Wedges\n1\n1 2 3 4 5 6\n$Media\n1\n1 1\n");
+  bool named = false;
+  try {
+    load_mesh(path);
+  } catch (const MeshError& e) {
+    named = std::string(e.what()).find("wedge 1") != std::string::npos;
+  }
+  CHECK(named);
+  // negative bulk modulus
+  write_text(path, "$Vertices\n6\n0 0 0\n1 0 0\n0 1 0\n0 0 1\n1 0 1\n0 1 1\n$Wedges\n1\n1 2 3 4 5 6\n$Media\n1\n1 -2\n");
+  CHECK_THROWS(load_mesh(path), MeshError);
+  // malformed record: error carries the line number
+  write_text(path, "$Vertices\n3\nnot a number\n");
+  bool lined = false;
+  try {
+    load_mesh(path);
+  } catch (const MeshError& e) {
+    lined = std::string(e.what()).find(":3") != std::string::npos;
+  }
+  CHECK(lined);
+  write_text(path, "$Bogus\n0\n");
+  CHECK_THROWS(load_mesh(path), MeshError);
+  CHECK_THROWS(load_mesh(tmp_file("pdg_no_such_dir/x.mesh")), MeshError);
+  std::remove(path.c_str());
+}
+
+TEST(surface_file_loads) {
+  const std::string path = tmp_file("pdg_surface.txt");
+  write_text(path, "$SurfaceVertices\n3\n0 0 0 1\n1 0 0 1\n0 1 0 1\n$SurfaceTriangles\n1\n1 2 3\n");
+  const SurfaceTriangulation s = load_surface(path);
+  CHECK(s.vertices.size() == 3);
+  CHECK(s.triangles.size() == 1);
+  const HybridMesh mesh = extrude_layer(s, 2);
+  CHECK(mesh.num_wedges() == 2);
+  CHECK_CLOSE(mesh_volume(mesh), 0.5, 1e-14);
+  std::remove(path.c_str());
+}
+
 // ---------------------------------------------------------------- solver via the CPU oracle
 TEST(oracle_zero_state_zero_rhs) {
   const Discretization d = small_box(1, 2);
