@@ -314,7 +314,7 @@ def measure_degree_dist(args, degree, ws, rank, local, peaks):
     t_setup = time.perf_counter()
     part = P.layered_slab(args.surface_n, [-1.0, -0.4, 0.2, 1.0], args.sublayers,
                           [(1.0, 1.0), (1.0, 4.0), (1.0, 2.25)], ws, rank)
-    solver = DistributedLSERK(part, degree, device=local, threads=os.cpu_count() or 1)
+    solver = DistributedLSERK(part, degree, device=local, threads=os.cpu_count() or 1, flags=pdg.capi.CTX_TIMING)
     d = solver.disc
     s = pdg.make_initial_state(d, "gaussian", [0.25, 0.0, 0.0, 0.0])
     dt = pdg.estimate_dt(d, 0.5)
@@ -325,6 +325,7 @@ def measure_degree_dist(args, degree, ws, rank, local, peaks):
     setup_s = time.perf_counter() - t_setup
     solver.step(dt, args.warmup)
     solver.synchronize()
+    solver.kernel_times(reset=True)
     dist.barrier()
     torch.cuda.synchronize()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -341,12 +342,44 @@ def measure_degree_dist(args, degree, ws, rank, local, peaks):
     tot = torch.tensor([owned_dofs], dtype=torch.float64, device="cuda")
     dist.all_reduce(tot)
     value = float(tot.item()) * args.steps / (ms / 1e3)
+    # roofline of this rank's wedge stage kernel: a stage is an interior and a boundary
+    # launch over disjoint owned elements, so per-stage time = summed launch time / stages
+    kt = solver.kernel_times(reset=True)
+    wbytes, _ = solver.stage_bytes()
+    stages = 5 * args.steps
+    stage_ms = kt["wedge_ms"] / stages if stages else 0.0
+    achieved = wbytes / (stage_ms / 1e3) / 1e9 if stage_ms > 0 else 0.0
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peaks[0], "unit": "GB/s", "frac": achieved / peaks[0],
+            "peak_source": peaks[1], "traffic": None, "algorithmic_bytes": wbytes,
+            "note": "rank 0; per stage = interior + boundary launch time"}
+    # e2e through the public API on every rank: pinned host state in, one step, state out
+    host = torch.empty(d.total_dofs, dtype=torch.float64, pin_memory=True)
+    hnp = host.numpy()
+    hnp[:] = s.u
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        solver.set_state(hnp)
+        solver.step(dt, 1)
+        solver.get_state(hnp)
+    el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    e2e = {"value": float(tot.item()) * e2e_steps / float(el.item()), "unit": UNIT,
+           "h2d_bytes_per_step": d.total_dofs * 8, "d2h_bytes_per_step": d.total_dofs * 8, "steps": e2e_steps,
+           "per_rank": True}
+    cnt = (C.c_int64 * 6)()
+    pdg.capi.check(pdg.capi.lib().pdg_partition_counts(solver.ctx, cnt))
+    interior, owned = cnt[4] + cnt[5], cnt[0] + cnt[1]
+    parts_nonempty = int(interior > 0) + int(owned - interior > 0)
     solver.close()
     return {"degree": degree, "value": value, "ms_per_step": ms / args.steps, "total_dofs": owned_dofs,
             "wedges": part.n_owned, "setup_s": round(setup_s, 1), "clocks": clk.summary(),
-            # per stage: interior + boundary wedge stage launches, one trace gather and
-            # one trace scatter per peer
-            "gpu_launches": args.steps * 5 * (2 + 2 * len(solver.peers)),
+            "roofline": roof, "e2e": e2e, "wedge_kernel_avg_ms": stage_ms,
+            # per stage: the non-empty interior / boundary stage launches, one trace gather
+            # and one trace scatter per peer
+            "gpu_launches": args.steps * 5 * (parts_nonempty + 2 * len(solver.peers)),
             "exchange_bytes_per_stage": solver.exchange_bytes}
 
 
@@ -367,6 +400,8 @@ def main():
     ap.add_argument("--workload", default="layered", choices=["layered", "hybrid"],
                     help="layered = configs[1] (1e6 wedges); hybrid = configs[2] (wedge layers over a tet cap)")
     ap.add_argument("--hybrid-n", type=int, default=64)
+    ap.add_argument("--partitioned", action="store_true",
+                    help="run the multi-GPU path (slab partition, DistributedLSERK, NCCL group) even at one GPU")
     ap.add_argument("--mass", default="exact", choices=["exact", "wadg"],
                     help="exact stored-lift mass (reference parity mode) or weight-adjusted (north-star WADG)")
     args = ap.parse_args()
@@ -379,10 +414,16 @@ def main():
     ws, rank, local = dist_env()
     import torch
     torch.cuda.set_device(local)
-    if ws > 1:
+    use_dist = ws > 1 or args.partitioned
+    if use_dist:
+        if ws == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29561")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks = load_peaks()
-    if ws > 1:
+    if use_dist:
         head = measure_degree_dist(args, args.degree, ws, rank, local, peaks)
         if rank == 0:
             line = {
@@ -396,7 +437,8 @@ def main():
                            "degree": args.degree, "wedges_per_gpu": head["wedges"],
                            "parallelism": f"mesh partition x{ws}", "l2": "inputs larger than L2, no flush",
                            "exchange_bytes_per_stage_per_rank": head["exchange_bytes_per_stage"]},
-                "roofline": None, "cpu_baseline": None, "e2e": None,
+                "roofline": head["roofline"], "cpu_baseline": None, "e2e": head["e2e"],
+                "wedge_kernel_avg_ms": head["wedge_kernel_avg_ms"],
                 "gpu_launches": head["gpu_launches"], "clocks": head["clocks"], "setup_s": head["setup_s"],
             }
             print(json.dumps(line), flush=True)

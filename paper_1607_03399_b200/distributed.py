@@ -42,16 +42,18 @@ def trace_offsets(ctx, elems, faces, per):
 
 class DistributedLSERK:
     def __init__(self, part, degree: int, device: int = 0, flux="upwind", mass="exact", threads=0,
-                 exchange="traces"):
+                 exchange="traces", flags=0, comm=None):
+        """flags: pdg_create flags (capi.CTX_TIMING for per-launch event timing); comm: the
+        point-to-point / all-reduce module, torch.distributed unless a test passes a stand-in"""
         import torch
         import torch.distributed as dist
 
-        self.torch, self.dist = torch, dist
+        self.torch, self.dist = torch, (comm if comm is not None else dist)
         self.part = part
         self.disc = S.build_discretization(part.mesh, degree, flux=flux, mass=mass, threads=threads)
         owned = np.ascontiguousarray(part.owned, dtype=np.uint8)
         h = C.c_void_p()
-        check(lib().pdg_create_partitioned(self.disc.handle, device, 0,
+        check(lib().pdg_create_partitioned(self.disc.handle, device, flags,
                                            owned.ctypes.data_as(C.POINTER(C.c_ubyte)), C.byref(h)))
         self.ctx = h
         counts = (C.c_int64 * 4)()
@@ -98,10 +100,24 @@ class DistributedLSERK:
         u = np.ascontiguousarray(u_local, dtype=np.float64)
         check(lib().pdg_set_state(self.ctx, C.c_void_p(u.ctypes.data), 0))
 
-    def get_state(self):
-        out = np.zeros(self.disc.total_dofs)
+    def get_state(self, out=None):
+        """local state in the reference layout; `out` may be a (pinned) float64 host array"""
+        if out is None:
+            out = np.zeros(self.disc.total_dofs)
         check(lib().pdg_get_state(self.ctx, C.c_void_p(out.ctypes.data), 0))
         return out
+
+    def kernel_times(self, reset=False):
+        wms, tms = C.c_double(), C.c_double()
+        wl, tl = C.c_int64(), C.c_int64()
+        check(lib().pdg_kernel_times(self.ctx, C.byref(wms), C.byref(wl), C.byref(tms), C.byref(tl), int(reset)))
+        return {"wedge_ms": wms.value, "wedge_launches": wl.value, "tet_ms": tms.value, "tet_launches": tl.value}
+
+    def stage_bytes(self):
+        """algorithmic bytes of one whole stage over the owned elements (5-stage average)"""
+        wb, tb = C.c_double(), C.c_double()
+        check(lib().pdg_stage_bytes(self.ctx, C.byref(wb), C.byref(tb)))
+        return wb.value, tb.value
 
     def _p2p(self):
         dist = self.dist
