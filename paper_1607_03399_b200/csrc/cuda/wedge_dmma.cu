@@ -66,6 +66,19 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #ifndef PDG_THREAD_CAP
 #define PDG_THREAD_CAP 384
 #endif
+// k permutation of the triangle products (G2/G3) at odd NT: in every block of four
+// k-steps lane (gid, tig) takes k = 16 b + 4 tig + s instead of 4 s + tig, so the
+// B reads {slice * stride + k} (odd stride) and the compact-L A reads {k * NT + i}
+// hit 16 distinct bank pairs per half-warp instead of 2-way conflicts; the tail
+// steps (4 KS not a multiple of 16) keep the contiguous order
+#ifndef PDG_KPERM
+#define PDG_KPERM 1
+#endif
+
+/// k index of lane column tig in k-step s (see PDG_KPERM)
+__host__ __device__ constexpr int kmap(int s, int tig, int KS, bool perm) {
+  return (perm && s < 4 * (KS / 4)) ? 16 * (s >> 2) + 4 * tig + (s & 3) : 4 * s + tig;
+}
 
 template <int N, int NST_>
 struct DCfg {
@@ -82,7 +95,8 @@ struct DCfg {
   static constexpr int USTR = r4(4 * NP) + 2;
   static constexpr int STAGE = r2(2 * USTR + LF + QF + WG + kWC / 2);
   // work buffers
-  static constexpr int VST = cf_stride(NT);                  // V row stride
+  static constexpr bool KP = PDG_KPERM && (NT & 1) && ST == NT; // permuted k (odd slice stride)
+  static constexpr int VST = KP ? NT : cf_stride(NT);        // V row stride (odd with KP)
   static constexpr int VS = r2((NPJ - 1) * VST + 4 * KS + 8);
   static constexpr int FQ = 3 * JT * KT * 32;                // fragment-major quad fluxes
   static constexpr int FTRI = r2(4 * KS + NT + 8);           // bottom/top tri fluxes (+ padding)
@@ -90,7 +104,7 @@ struct DCfg {
   // padded copy of the state for bank-conflict-free fragment loads when NT is
   // not 4 or 12 mod 16 (row = field*NQ + slice, stride SP)
   // measured: N = 4 3.93 vs 4.22 ms, N = 5 6.55 vs 6.31 ms (profiles/round1_pad_state_ab.txt)
-  static constexpr bool PAD = PDG_PAD_STATE && cf_stride(NT) != NT && N == 4;
+  static constexpr bool PAD = PDG_PAD_STATE && cf_stride(NT) != NT && N == 4 && !KP;
   static constexpr int SP = PAD ? cf_stride(NT) : ST;
   static constexpr int UPS = PAD ? r2((4 * NQ + 8 * JT + 4 * KT) * SP + 4 * KS + 8) : 0;
   static constexpr int WORK = VS + 2 * (FTRI + FQ) + ZS + UPS;
@@ -162,7 +176,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
   extern __shared__ __align__(16) double smem[];
 
   // ---- shared reference tables (fragment-major, zero padded) ----------------
-  double* sDr = smem;                        // [t][s][lane] = Dr(8t+gid, 4s+tig)
+  double* sDr = smem;                        // [t][s][lane] = Dr(8t+gid, kmap(s, tig))
   double* sDs = sDr + C::IT * KS * 32;
   double* sDt = sDs + C::IT * KS * 32;       // [jt][s][lane] = Dt(8jt+gid, 4s+tig)
   double* sProf = sDt + JT * KT * 32;        // [2][NQ]
@@ -172,7 +186,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
   __syncthreads();
   for (int q = threadIdx.x; q < C::IT * KS * 32; q += C::THREADS) {
     const int lane = q & 31, ts = q >> 5, t = ts / KS, s = ts - t * KS;
-    const int i = 8 * t + (lane >> 2), k = 4 * s + (lane & 3);
+    const int i = 8 * t + (lane >> 2), k = kmap(s, lane & 3, KS, C::KP);
     if (i < NT && k < NT) {
       sDr[q] = p.DrT[k * NT + i];
       sDs[q] = p.DsT[k * NT + i];
@@ -402,7 +416,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
       for (int jt = 0; jt < JTL; ++jt) lp[jt][0] = lp[jt][1] = 0.0;
 #pragma unroll
       for (int s2 = 0; s2 < KS; ++s2) {
-        const int k = 4 * s2 + tig;
+        const int k = kmap(s2, tig, KS, C::KP);
         const int fo = ((t * KS + s2) << 5) + lane;
 #if PDG_COMPACT_OPS
         const double la = (i < NT && k < NT) ? Lf[k * NT + i] : 0.0;
