@@ -66,6 +66,13 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #ifndef PDG_THREAD_CAP
 #define PDG_THREAD_CAP 384
 #endif
+// no end-of-element team barrier: the flux buffers alternate with the element
+// parity and the next element's TMA copy is issued after the flux barrier (when
+// every warp of the team has left the previous element), so one barrier per
+// element goes
+#ifndef PDG_NO_END_BARRIER
+#define PDG_NO_END_BARRIER 1
+#endif
 // k permutation of the triangle products (G2/G3) at odd NT: in every block of four
 // k-steps lane (gid, tig) takes k = 16 b + 4 tig + s instead of 4 s + tig, so the
 // B reads {slice * stride + k} (odd stride) and the compact-L A reads {k * NT + i}
@@ -107,12 +114,17 @@ struct DCfg {
   static constexpr bool PAD = PDG_PAD_STATE && cf_stride(NT) != NT && N == 4 && !KP;
   static constexpr int SP = PAD ? cf_stride(NT) : ST;
   static constexpr int UPS = PAD ? r2((4 * NQ + 8 * JT + 4 * KT) * SP + 4 * KS + 8) : 0;
-  static constexpr int WORK = VS + 2 * (FTRI + FQ) + ZS + UPS;
+  static constexpr int FB = 2 * (FTRI + FQ);                 // one set of flux buffers
+  // measured (profiles/round1_noend_ab.txt): N = 4 -0.5%, N = 5 -1.5%, N = 6 even,
+  // N = 7 +6% (shorter prefetch lead), so on at N <= 5 only
+  static constexpr int FBUF = (PDG_NO_END_BARRIER && !PAD && NST_ == 2 && N <= 5) ? 2 : 1;
+  static constexpr int WORK = VS + FBUF * FB + ZS + UPS;
   static constexpr int TABLES = r2(2 * IT * KS * 32 + JT * KT * 32 + 2 * NQ + ceil_div(FW, 2) + kComboCap / 2);
   static constexpr int SMEM_BUDGET = 225 * 1024;
   // double-buffered stages unless even a single team would not fit
   static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 6 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
   static constexpr int PER_TEAM = 6 + NSTAGE * STAGE + WORK;
+  static constexpr bool NOEND = FBUF == 2 && NSTAGE == 2;
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
   // <= PDG_THREAD_CAP threads per CTA: 384 keeps >= 168 registers per thread
   // (profiles/round1_compact_ops_ab.txt: compact operators + 384 beat 512)
@@ -211,12 +223,9 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
   uint64_t* bar = reinterpret_cast<uint64_t*>(tbase);
   double* stg0 = tbase + 6; // 2 mbarriers + 3 schedule slots + pad
   double* V = stg0 + NST * C::STAGE;
-  double* Ftp = V + C::VS;      // tri-face fluxes: p part [2][NT]
-  double* Ftu = Ftp + C::FTRI;  //                  u part
-  double* Fqp = Ftu + C::FTRI;  // quad-face fluxes, fragment-major [f][jt][s][lane]
-  double* Fqu = Fqp + C::FQ;
-  const double* Zero = Fqu + C::FQ; // ZS zeros, never written
-  double* Upad = Fqu + C::FQ + C::ZS; // padded state copy (C::PAD)
+  double* const Fbase = V + C::VS; // C::FBUF sets of flux buffers (element parity)
+  const double* Zero = Fbase + C::FBUF * C::FB; // ZS zeros, never written
+  double* Upad = Fbase + C::FBUF * C::FB + C::ZS; // padded state copy (C::PAD)
   constexpr int SP = C::SP;
   if (tt == 0) {
     mbar_init(bar, 1);
@@ -317,7 +326,11 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
     const double* Qf = Lf + C::LF;
     const double* G = Qf + C::QF;
     const int* Cn = reinterpret_cast<const int*>(G + WG);
-    if (NST == 2 && tt == 0 && en < p.Kw_active) {
+    double* Ftp = Fbase + (C::NOEND ? (n & 1) * C::FB : 0); // tri-face fluxes: p part [2][NT]
+    double* Ftu = Ftp + C::FTRI;                              //                  u part
+    double* Fqp = Ftu + C::FTRI; // quad-face fluxes, fragment-major [f][jt][s][lane]
+    double* Fqu = Fqp + C::FQ;
+    if (NST == 2 && !C::NOEND && tt == 0 && en < p.Kw_active) {
       fence_proxy_async_smem();
       load_element<N, NST>(p, stg0 + (s ^ 1) * C::STAGE, en, res_src, bar + (s ^ 1));
     }
@@ -365,6 +378,11 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
       }
     }
     team_sync(bar_id, 32 * T);
+    // every warp of the team has left the previous element: its stage may be refilled
+    if (C::NOEND && tt == 0 && en < p.Kw_active) {
+      fence_proxy_async_smem();
+      load_element<N, NST>(p, stg0 + (s ^ 1) * C::STAGE, en, res_src, bar + (s ^ 1));
+    }
 
     // ---- G1: V[j][i] for row tile w, with the bottom/top pressure lifts folded in
     {
@@ -553,7 +571,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
           }
         }
     }
-    team_sync(bar_id, 32 * T); // stage s and the work buffers are free again
+    if (!C::NOEND) team_sync(bar_id, 32 * T); // stage s and the work buffers are free again
     if (NST == 1 && tt == 0 && en < p.Kw_active) load_element<N, NST>(p, stg0, en, res_src, bar);
     e = slot[1 + (n & 1)];
   }
