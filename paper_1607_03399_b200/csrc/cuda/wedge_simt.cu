@@ -95,6 +95,11 @@ __host__ __device__ constexpr int slot_stride(int x, int NT, int H) {
 #endif
 #endif
 
+// the WADG variant has no slice split: min 3 CTAs/SM at N = 1 (4 spills), 1 above
+#ifndef PDG_WADG_SIMT_MINB
+#define PDG_WADG_SIMT_MINB(N) ((N) == 1 ? 3 : 1)
+#endif
+
 template <int N, bool WADG = false>
 struct SCfg {
   static_assert(nts_of(N) == nt_of(N), "the low-order kernel assumes an unpadded slice stride");
@@ -155,7 +160,8 @@ __device__ __forceinline__ void load_chunk(const StageParams& p, double* stg, lo
 }
 
 template <int N, bool WADG>
-__global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, PDG_SIMT_MINB(N)) wedge_simt_kernel(const StageParams p) {
+__global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, WADG ? PDG_WADG_SIMT_MINB(N) : PDG_SIMT_MINB(N))
+    wedge_simt_kernel(const StageParams p) {
   using C = SCfg<N, WADG>;
   constexpr int NQ = C::NQ, NT = C::NT, NP = C::NP, FW = C::FW, WG = C::WG, E = C::E;
   constexpr int SU = C::SU, SG = C::SG, SF = C::SF, SV = C::SV;
