@@ -49,6 +49,21 @@ constexpr int kComboCapW = 2048; // ints of neighbour node maps kept in shared m
 #ifndef PDG_WADG_PAD_STATE
 #define PDG_WADG_PAD_STATE 1
 #endif
+// permuted k order of the K-folded gradient products at odd NT and no
+// end-of-element barrier (parity flux / 1/J buffers): see PDG_KPERM and
+// PDG_NO_END_BARRIER in wedge_dmma.cu
+#ifndef PDG_WADG_KPERM
+#define PDG_WADG_KPERM 1
+#endif
+#ifndef PDG_WADG_NO_END_BARRIER
+#define PDG_WADG_NO_END_BARRIER 1
+#endif
+#ifndef PDG_WADG_NOEND_MAX_N
+#define PDG_WADG_NOEND_MAX_N 7
+#endif
+__host__ __device__ constexpr int wkmap(int s, int tig, int KS, bool perm) {
+  return (perm && s < 4 * (KS / 4)) ? 16 * (s >> 2) + 4 * tig + (s & 3) : 4 * s + tig;
+}
 // threads per CTA: 384 (>= 168 registers) at N <= 6, 512 at N = 7 (global tables)
 // -- measured, profiles/round1_wadg_tables.txt
 #ifndef PDG_WADG_THREAD_CAP
@@ -84,13 +99,17 @@ struct WCfg {
   static constexpr int IJ = r2(4 * KQ);                      // 1/J at the cubature points
   // padded state copy for bank-conflict-free fragment loads (see wedge_dmma.cu)
   // measured: N = 4 5.05 -> 4.60 ms, N = 5 8.59 -> 8.86 ms (profiles/round1_pad_state_ab.txt)
-  static constexpr bool PAD = PDG_WADG_PAD_STATE && cf_stride(NT) != NT && N == 4;
+  static constexpr bool KP = PDG_WADG_KPERM && (NT & 1) && ST == NT;
+  static constexpr bool PAD = PDG_WADG_PAD_STATE && cf_stride(NT) != NT && N == 4 && !KP;
   static constexpr int SP = PAD ? cf_stride(NT) : ST;
   static constexpr int UPS = PAD ? r2((4 * NQ + 8 * JT + 4 * KT) * SP + 4 * KS + 8) : 0;
-  static constexpr int WORK = BS + 2 * (FTRI + FQ) + IJ + UPS;
+  static constexpr int FBW = 2 * (FTRI + FQ) + IJ; // flux buffers + 1/J, one element
+  static constexpr int FBUF = (PDG_WADG_NO_END_BARRIER && !PAD && NST_ == 2 && N <= PDG_WADG_NOEND_MAX_N) ? 2 : 1;
+  static constexpr int WORK = BS + FBUF * FBW + UPS;
   static constexpr int SMEM_BUDGET = 225 * 1024;
   static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 6 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
   static constexpr int PER_TEAM = 6 + NSTAGE * STAGE + WORK;
+  static constexpr bool NOEND = FBUF == 2 && NSTAGE == 2;
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
   static constexpr int TPB = cmax(1, cmin(cmin(15, PDG_WADG_THREAD_CAP(N) / (32 * T)), TPB_SMEM)); // teams per CTA
   static constexpr int THREADS = 32 * T * TPB;
@@ -136,7 +155,7 @@ __device__ void fill_wadg_tables(double* dst, const double* W, int tid, int nthr
   for (int q = tid; q < 6 * C::KDT; q += nthr) {
     const int lane = q & 31, rest = q >> 5;
     const int s = rest % KS, t = (rest / KS) % IT, m = rest / (KS * IT);
-    const int i = 8 * t + (lane >> 2), k = 4 * s + (lane & 3);
+    const int i = 8 * t + (lane >> 2), k = wkmap(s, lane & 3, KS, C::KP);
     sKD[q] = (i < NT && k < NT) ? W[(m * NT + i) * NT + k] : 0.0;
   }
   for (int q = tid; q < C::PQT; q += nthr) {
@@ -226,12 +245,8 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
   uint64_t* bar = reinterpret_cast<uint64_t*>(tbase);
   double* stg0 = tbase + 6; // 2 mbarriers + 3 schedule slots + pad
   double* Bb = stg0 + NST * C::STAGE; // pre-lift buffer, column n = field*NQ + j, row = tri node
-  double* Ftp = Bb + C::BS;           // [2][NT]
-  double* Ftu = Ftp + C::FTRI;
-  double* Fqp = Ftu + C::FTRI;        // [f][jt][s][lane]
-  double* Fqu = Fqp + C::FQ;
-  double* sIJ = Fqu + C::FQ;          // [4 KQ], zero beyond NC
-  double* Upad = sIJ + C::IJ;         // padded state copy (C::PAD)
+  double* const Fbase = Bb + C::BS;   // C::FBUF sets of {Ftp, Ftu, Fqp, Fqu, 1/J} (element parity)
+  double* Upad = Fbase + C::FBUF * C::FBW; // padded state copy (C::PAD)
   constexpr int SP = C::SP;
   if (tt == 0) {
     mbar_init(bar, 1);
@@ -296,7 +311,12 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
     const double* R = U + C::USTR;
     const double* G = R + C::USTR;
     const int* Cn = reinterpret_cast<const int*>(G + WG);
-    if (NST == 2 && tt == 0 && en < p.Kw_active) {
+    double* Ftp = Fbase + (C::NOEND ? (n & 1) * C::FBW : 0); // [2][NT]
+    double* Ftu = Ftp + C::FTRI;
+    double* Fqp = Ftu + C::FTRI; // [f][jt][s][lane]
+    double* Fqu = Fqp + C::FQ;
+    double* sIJ = Fqu + C::FQ;   // [4 KQ], zero beyond NC
+    if (NST == 2 && !C::NOEND && tt == 0 && en < p.Kw_active) {
       fence_proxy_async_smem();
       load_element<N, NST>(p, stg0 + (s ^ 1) * C::STAGE, en, res_src, bar + (s ^ 1));
     }
@@ -369,6 +389,11 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
     }
     for (int q = tt; q < NC; q += 32 * T) sIJ[q] = 1.0 / (j0 + jr * sQr[q] + js * sQs[q]);
     team_sync(bar_id, 32 * T);
+    // every warp of the team has left the previous element: its stage may be refilled
+    if (C::NOEND && tt == 0 && en < p.Kw_active) {
+      fence_proxy_async_smem();
+      load_element<N, NST>(p, stg0 + (s ^ 1) * C::STAGE, en, res_src, bar + (s ^ 1));
+    }
 
     const int t = w;
     const int i = 8 * t + gid;
@@ -395,7 +420,7 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
       const double cy[6] = {ry * j0, ry * jr, ry * js, sym * j0, sym * jr, sym * js};
 #pragma unroll
       for (int s2 = 0; s2 < KS; ++s2) {
-        const int k = 4 * s2 + tig;
+        const int k = wkmap(s2, tig, KS, C::KP);
         const int fo = ((t * KS + s2) << 5) + lane;
         double ax = 0.0, ay = 0.0;
 #pragma unroll
@@ -549,7 +574,7 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
           }
         }
     }
-    team_sync(bar_id, 32 * T); // stage s and the work buffers are free again
+    if (!C::NOEND) team_sync(bar_id, 32 * T); // stage s and the work buffers are free again
     if (NST == 1 && tt == 0 && en < p.Kw_active) load_element<N, NST>(p, stg0, en, res_src, bar);
     e = slot[1 + (n & 1)];
   }

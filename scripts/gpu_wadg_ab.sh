@@ -1,0 +1,16 @@
+# WADG DMMA kernel: k order + no end barrier (_lib), k order only (_lib_wk), neither (_lib_w0); same box, alternating
+summ() { python - "$1" <<'PY'
+import json,sys
+try: d=json.loads(open(sys.argv[1]).read())
+except Exception as e: print("fail"); sys.exit()
+rows=[{'degree':d['config']['degree'],'wedge_kernel_avg_ms':d['wedge_kernel_avg_ms']}]+d.get('sweep',[])
+print(" ".join(f"N{r['degree']}:{r['wedge_kernel_avg_ms']:.3f}" for r in sorted(rows,key=lambda r:r['degree'])))
+PY
+}
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_wadg.py tests/test_ab3.py tests/test_gpu_edge_cases.py -m gpu -q -p no:cacheprovider > gpurun_out/wab_pytest.log 2>&1; echo "pytest exit $?"; tail -1 gpurun_out/wab_pytest.log
+for rep in 1 2; do
+for v in _lib _lib_wk _lib_w0; do
+PDG_LIB_PATH=$PWD/paper_1607_03399_b200/$v/libprismdg_b200.so timeout 900 python bench.py --mass wadg --steps 5 --warmup 3 --degree 5 --degrees 4,6,7 --no-cpu-baseline --e2e-steps 1 > gpurun_out/wab_$v.json 2> gpurun_out/wab_$v.err; echo "$v $(summ gpurun_out/wab_$v.json)"
+done
+done
