@@ -65,6 +65,12 @@ __host__ __device__ constexpr int slot_stride(int x, int NT, int H) {
   return best;
 }
 
+// the chunk-start barrier (needed anyway: cp.async completion is per thread) also
+// proves every thread has left the previous chunk, so the next chunk's copy is
+// issued right after it and the end-of-chunk barrier goes
+#ifndef PDG_SIMT_NO_END_BARRIER
+#define PDG_SIMT_NO_END_BARRIER 1
+#endif
 #ifndef PDG_SIMT_THREADS
 #define PDG_SIMT_THREADS 128
 #endif
@@ -124,6 +130,9 @@ struct SCfg {
   static constexpr int TABLES = r2(r2(2 * NT * NT + NQ * NQ + 2 * NQ + WTAB) + ceil_div(FW, 2) + 2048 / 2);
   static constexpr size_t SMEM_BYTES = (size_t)8 * (TABLES + 2 * STAGE + E * (SF + SV) + 4);
   static constexpr int TASKS = ceil_div(E * FW, THREADS);
+  // measured (profiles/round1_simt_noend_ab.txt): exact N = 1 -5.5%, N = 3 -1.8%,
+  // N = 2 +1%; WADG N = 2 -4.1%, N = 3 -5.2%, N = 1 +2.5%
+  static constexpr bool NOEND = PDG_SIMT_NO_END_BARRIER && (WADG ? N >= 2 : N != 2);
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -241,13 +250,22 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, WADG ? PDG_WADG_SIMT_M
     double* cur = stg + (it & 1) * C::STAGE;
     // prefetch the next chunk into the other stage (it was released by the
     // trailing barrier of the previous iteration)
-    if (cn < nchunk) load_chunk<N, WADG>(p, stg + ((it + 1) & 1) * C::STAGE, p.Kw_begin + cn * E, nel_of(cn));
-    cp_async_commit();
-    cp_async_wait<1>();
+    if (!C::NOEND) {
+      if (cn < nchunk) load_chunk<N, WADG>(p, stg + ((it + 1) & 1) * C::STAGE, p.Kw_begin + cn * E, nel_of(cn));
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
     // next ticket; the slot alternates with the iteration parity so it is never
     // rewritten before every thread has read it
     if (threadIdx.x == 0) slot[2 + (it & 1)] = (long long)(atomicAdd(p.ticket, 1ULL) - p.ticket_base);
     __syncthreads();
+    // every thread has left the previous chunk: its stage takes the next one
+    if (C::NOEND) {
+      if (cn < nchunk) load_chunk<N, WADG>(p, stg + ((it + 1) & 1) * C::STAGE, p.Kw_begin + cn * E, nel_of(cn));
+      cp_async_commit();
+    }
     const long long e0 = p.Kw_begin + c * E;
     const int nel = nel_of(c);
     const double* sU = cur;
@@ -644,7 +662,7 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, WADG ? PDG_WADG_SIMT_M
         }
     }
     }
-    __syncthreads(); // the stage and the work buffers are free again
+    if (!C::NOEND) __syncthreads(); // the stage and the work buffers are free again
     c = cn;
     cn = slot[2 + (it & 1)];
   }
