@@ -73,6 +73,12 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #ifndef PDG_NO_END_BARRIER
 #define PDG_NO_END_BARRIER 1
 #endif
+// volume products first: the metric-folded gradient / divergence products (G2's
+// volume half) and the vertical product of G1 need only the element's own state,
+// so they run between issuing the neighbour-trace gathers and using them
+#ifndef PDG_VOL_FIRST
+#define PDG_VOL_FIRST 1
+#endif
 // k permutation of the triangle products (G2/G3) at odd NT: in every block of four
 // k-steps lane (gid, tig) takes k = 16 b + 4 tig + s instead of 4 s + tig, so the
 // B reads {slice * stride + k} (odd stride) and the compact-L A reads {k * NT + i}
@@ -125,6 +131,9 @@ struct DCfg {
   static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 6 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
   static constexpr int PER_TEAM = 6 + NSTAGE * STAGE + WORK;
   static constexpr bool NOEND = FBUF == 2 && NSTAGE == 2;
+  // measured (profiles/round1_volfirst_ab.txt): N = 4 -2.8%, N = 6 -4.5%, N = 7 -6.5%,
+  // N = 5 +0.4% (with the dropped end barrier its gathers are already covered)
+  static constexpr bool VF = PDG_VOL_FIRST && N != 5;
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
   // <= PDG_THREAD_CAP threads per CTA: 384 keeps >= 168 registers per thread
   // (profiles/round1_compact_ops_ab.txt: compact operators + 384 beat 512)
@@ -344,9 +353,54 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
       }
     const double* Us = C::PAD ? Upad : U; // state with row stride SP
 
+    // ---- volume products (C::VF): only the state, while the gathers are in flight
+    double gx[JT][2], gy[JT][2], dvx[JT][2], dvy[JT][2], dg1[JT][2];
+#pragma unroll
+    for (int jt = 0; jt < JT; ++jt)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) gx[jt][c] = gy[jt][c] = dvx[jt][c] = dvy[jt][c] = dg1[jt][c] = 0.0;
+    if (C::VF) {
+      if (surf) gather(Cn);
+      if (vol) {
+        const int i = 8 * w + gid;
+        const double tzJ = G[W_TZJ];
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt) {
+          const int jb = 8 * jt + gid;
+          const int jc = jb < NQ ? jb : NQ - 1;
+          const double sx_ = G[W_TXJ + jc], sy_ = G[w_tyj(N) + jc];
+#pragma unroll
+          for (int s2 = 0; s2 < KT; ++s2) {
+            const int l = 4 * s2 + tig;
+            const double bd = sDt[((jt * KT + s2) << 5) + lane];
+            dmma(dg1[jt], Us[(NQ + l) * SP + i], sx_ * bd);
+            dmma(dg1[jt], Us[(2 * NQ + l) * SP + i], sy_ * bd);
+            dmma(dg1[jt], Us[(3 * NQ + l) * SP + i], tzJ * bd);
+          }
+        }
+        const double rx = G[W_RX], ry = G[W_RY], sxm = G[W_SX], sym = G[W_SY];
+#pragma unroll
+        for (int s2 = 0; s2 < KS; ++s2) {
+          const int k = kmap(s2, tig, KS, C::KP);
+          const int fo = ((w * KS + s2) << 5) + lane;
+          const double dr = sDr[fo], ds = sDs[fo];
+          const double cx = rx * dr + sxm * ds, cy = ry * dr + sym * ds;
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) {
+            const int jb = 8 * jt + gid;
+            const double bp = jb < NQ ? Us[jb * SP + k] : 0.0; // padding columns are discarded
+            dmma(gx[jt], cx, bp);
+            dmma(gy[jt], cy, bp);
+            dmma(dvx[jt], cx, Us[(NQ + jb) * SP + k]);
+            dmma(dvy[jt], cy, Us[(2 * NQ + jb) * SP + k]);
+          }
+        }
+      }
+    }
+
     // ---- numerical fluxes on all face nodes -------------------------------------
     if (surf) {
-      gather(Cn);
+      if (!C::VF) gather(Cn);
 #pragma unroll
       for (int q = 0; q < QL_; ++q) {
         const int f = task_f[q];
@@ -391,8 +445,8 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
       const double fb = surf ? jfb * Ftp[i] : 0.0, ftop = surf ? jft * Ftp[NT + i] : 0.0;
 #pragma unroll
       for (int jt = 0; jt < JT; ++jt) {
-        double d[2] = {0.0, 0.0};
-        if (vol) {
+        double d[2] = {dg1[jt][0], dg1[jt][1]};
+        if (vol && !C::VF) {
           const int jb = 8 * jt + gid;
           const int jc = jb < NQ ? jb : NQ - 1;
           const double sx_ = G[W_TXJ + jc], sy_ = G[w_tyj(N) + jc];
@@ -425,11 +479,9 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
         const int nc = 8 * jt + gid;
         src[jt] = nc < NQ ? Us + nc * SP : (nc == NQ ? Ftu : (nc == NQ + 1 ? Ftu + NT : Zero));
       }
-      double gx[JT][2], gy[JT][2], dvx[JT][2], dvy[JT][2], lv[JT][2], lp[JTL][2];
+      double lv[JT][2], lp[JTL][2];
 #pragma unroll
-      for (int jt = 0; jt < JT; ++jt)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) gx[jt][c] = gy[jt][c] = dvx[jt][c] = dvy[jt][c] = lv[jt][c] = 0.0;
+      for (int jt = 0; jt < JT; ++jt) lv[jt][0] = lv[jt][1] = 0.0;
 #pragma unroll
       for (int jt = 0; jt < JTL; ++jt) lp[jt][0] = lp[jt][1] = 0.0;
 #pragma unroll
@@ -442,7 +494,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
         const double la = Lf[fo];
 #endif
         double cx = 0.0, cy = 0.0;
-        if (vol) {
+        if (vol && !C::VF) {
           const double dr = sDr[fo], ds = sDs[fo];
           cx = rx * dr + sxm * ds;
           cy = ry * dr + sym * ds;
@@ -453,7 +505,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
           dmma(lp[jt], la, bp);
           if (jt < JT) {
             const int jb = 8 * jt + gid;
-            if (vol) {
+            if (vol && !C::VF) {
               dmma(gx[jt], cx, bp);
               dmma(gy[jt], cy, bp);
               dmma(dvx[jt], cx, Us[(NQ + jb) * SP + k]);
