@@ -73,6 +73,9 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #ifndef PDG_NO_END_BARRIER
 #define PDG_NO_END_BARRIER 1
 #endif
+#ifndef PDG_NOEND_MAX_N
+#define PDG_NOEND_MAX_N 5
+#endif
 // volume products first: the metric-folded gradient / divergence products (G2's
 // volume half) and the vertical product of G1 need only the element's own state,
 // so they run between issuing the neighbour-trace gathers and using them
@@ -123,7 +126,7 @@ struct DCfg {
   static constexpr int FB = 2 * (FTRI + FQ);                 // one set of flux buffers
   // measured (profiles/round1_noend_ab.txt): N = 4 -0.5%, N = 5 -1.5%, N = 6 even,
   // N = 7 +6% (shorter prefetch lead), so on at N <= 5 only
-  static constexpr int FBUF = (PDG_NO_END_BARRIER && !PAD && NST_ == 2 && N <= 5) ? 2 : 1;
+  static constexpr int FBUF = (PDG_NO_END_BARRIER && !PAD && NST_ == 2 && N <= PDG_NOEND_MAX_N) ? 2 : 1;
   static constexpr int WORK = VS + FBUF * FB + ZS + UPS;
   static constexpr int TABLES = r2(2 * IT * KS * 32 + JT * KT * 32 + 2 * NQ + ceil_div(FW, 2) + kComboCap / 2);
   static constexpr int SMEM_BUDGET = 225 * 1024;

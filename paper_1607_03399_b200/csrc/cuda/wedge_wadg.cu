@@ -58,6 +58,11 @@ constexpr int kComboCapW = 2048; // ints of neighbour node maps kept in shared m
 #ifndef PDG_WADG_NO_END_BARRIER
 #define PDG_WADG_NO_END_BARRIER 1
 #endif
+// K-folded gradient and vertical products (phases B, C) before the flux phase,
+// between issuing the neighbour gathers and using them
+#ifndef PDG_WADG_VOL_FIRST
+#define PDG_WADG_VOL_FIRST 1
+#endif
 #ifndef PDG_WADG_NOEND_MAX_N
 #define PDG_WADG_NOEND_MAX_N 7
 #endif
@@ -110,6 +115,8 @@ struct WCfg {
   static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 6 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
   static constexpr int PER_TEAM = 6 + NSTAGE * STAGE + WORK;
   static constexpr bool NOEND = FBUF == 2 && NSTAGE == 2;
+  // measured (profiles/round1_volfirst_ab.txt): N = 4 -1.2%, N = 7 -2.4%, N = 5 +5.7%, N = 6 +4.3%
+  static constexpr bool VF = PDG_WADG_VOL_FIRST && (N == 4 || N == 7);
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
   static constexpr int TPB = cmax(1, cmin(cmin(15, PDG_WADG_THREAD_CAP(N) / (32 * T)), TPB_SMEM)); // teams per CTA
   static constexpr int THREADS = 32 * T * TPB;
@@ -330,6 +337,66 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
       }
     const double* Us = C::PAD ? Upad : U; // state with row stride SP, published by the flux barrier
 
+    // ---- B, C (volume products; before the fluxes with PDG_WADG_VOL_FIRST) -------
+    double gx[JT][2], gy[JT][2], dvx[JT][2], dvy[JT][2];
+    double vp[JT][2], pdt[JT][2];
+    const double tzJ = G[W_TZJ];
+    auto vol_products = [&]() {
+      const int iw = 8 * w + gid;
+    // ---- B: K-folded gradients gx, gy and divergence parts dvx, dvy ----------
+#pragma unroll
+    for (int jt = 0; jt < JT; ++jt)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) gx[jt][c] = gy[jt][c] = dvx[jt][c] = dvy[jt][c] = 0.0;
+    if (vol) {
+      const double rx = G[W_RX], ry = G[W_RY], sxm = G[W_SX], sym = G[W_SY];
+      const double cx[6] = {rx * j0, rx * jr, rx * js, sxm * j0, sxm * jr, sxm * js};
+      const double cy[6] = {ry * j0, ry * jr, ry * js, sym * j0, sym * jr, sym * js};
+#pragma unroll
+      for (int s2 = 0; s2 < KS; ++s2) {
+        const int k = wkmap(s2, tig, KS, C::KP);
+        const int fo = ((w * KS + s2) << 5) + lane;
+        double ax = 0.0, ay = 0.0;
+#pragma unroll
+        for (int m = 0; m < 6; ++m) {
+          const double d = tab(tKD, m * C::KDT + fo);
+          ax += cx[m] * d;
+          ay += cy[m] * d;
+        }
+#pragma unroll
+        for (int jt = 0; jt < JT; ++jt) {
+          const int jb = 8 * jt + gid;
+          const double bp = Us[jb * SP + k];
+          dmma(gx[jt], ax, bp);
+          dmma(gy[jt], ay, bp);
+          dmma(dvx[jt], ax, Us[(NQ + jb) * SP + k]);
+          dmma(dvy[jt], ay, Us[(2 * NQ + jb) * SP + k]);
+        }
+      }
+    }
+
+    // ---- C: vertical terms vp = txJ Dt UX + tyJ Dt UY + tzJ Dt UZ, pdt = P Dt^T
+#pragma unroll
+    for (int jt = 0; jt < JT; ++jt) vp[jt][0] = vp[jt][1] = pdt[jt][0] = pdt[jt][1] = 0.0;
+    if (vol) {
+#pragma unroll
+      for (int jt = 0; jt < JT; ++jt) {
+        const int jb = 8 * jt + gid;
+        const int jc = jb < NQ ? jb : NQ - 1;
+        const double sx_ = G[W_TXJ + jc], sy_ = G[w_tyj(N) + jc];
+#pragma unroll
+        for (int s2 = 0; s2 < KT; ++s2) {
+          const int l = 4 * s2 + tig;
+          const double bd = sDt[((jt * KT + s2) << 5) + lane];
+          dmma(vp[jt], Us[(NQ + l) * SP + iw], sx_ * bd);
+          dmma(vp[jt], Us[(2 * NQ + l) * SP + iw], sy_ * bd);
+          dmma(vp[jt], Us[(3 * NQ + l) * SP + iw], tzJ * bd);
+          dmma(pdt[jt], Us[l * SP + iw], bd);
+        }
+      }
+    }
+
+    };
     // ---- numerical fluxes on all face nodes; 1/J at the cubature points -------
     if (surf) {
       double nb[QL_][4];
@@ -357,6 +424,7 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
           }
         }
       }
+      if (C::VF) vol_products(); // while the gathers are in flight
 #pragma unroll
       for (int q = 0; q < QL_; ++q) {
         const int f = task_f[q];
@@ -387,6 +455,7 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
         }
       }
     }
+    if (C::VF && !surf) vol_products();
     for (int q = tt; q < NC; q += 32 * T) sIJ[q] = 1.0 / (j0 + jr * sQr[q] + js * sQs[q]);
     team_sync(bar_id, 32 * T);
     // every warp of the team has left the previous element: its stage may be refilled
@@ -408,61 +477,7 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
       for (int ct = 0; ct < IT; ++ct) dmma(lt[ct], a, tab(tVq, ((ct * KQ + s2) << 5) + lane));
     }
 
-    // ---- B: K-folded gradients gx, gy and divergence parts dvx, dvy ----------
-    double gx[JT][2], gy[JT][2], dvx[JT][2], dvy[JT][2];
-#pragma unroll
-    for (int jt = 0; jt < JT; ++jt)
-#pragma unroll
-      for (int c = 0; c < 2; ++c) gx[jt][c] = gy[jt][c] = dvx[jt][c] = dvy[jt][c] = 0.0;
-    if (vol) {
-      const double rx = G[W_RX], ry = G[W_RY], sxm = G[W_SX], sym = G[W_SY];
-      const double cx[6] = {rx * j0, rx * jr, rx * js, sxm * j0, sxm * jr, sxm * js};
-      const double cy[6] = {ry * j0, ry * jr, ry * js, sym * j0, sym * jr, sym * js};
-#pragma unroll
-      for (int s2 = 0; s2 < KS; ++s2) {
-        const int k = wkmap(s2, tig, KS, C::KP);
-        const int fo = ((t * KS + s2) << 5) + lane;
-        double ax = 0.0, ay = 0.0;
-#pragma unroll
-        for (int m = 0; m < 6; ++m) {
-          const double d = tab(tKD, m * C::KDT + fo);
-          ax += cx[m] * d;
-          ay += cy[m] * d;
-        }
-#pragma unroll
-        for (int jt = 0; jt < JT; ++jt) {
-          const int jb = 8 * jt + gid;
-          const double bp = Us[jb * SP + k];
-          dmma(gx[jt], ax, bp);
-          dmma(gy[jt], ay, bp);
-          dmma(dvx[jt], ax, Us[(NQ + jb) * SP + k]);
-          dmma(dvy[jt], ay, Us[(2 * NQ + jb) * SP + k]);
-        }
-      }
-    }
-
-    // ---- C: vertical terms vp = txJ Dt UX + tyJ Dt UY + tzJ Dt UZ, pdt = P Dt^T
-    const double tzJ = G[W_TZJ];
-    double vp[JT][2], pdt[JT][2];
-#pragma unroll
-    for (int jt = 0; jt < JT; ++jt) vp[jt][0] = vp[jt][1] = pdt[jt][0] = pdt[jt][1] = 0.0;
-    if (vol) {
-#pragma unroll
-      for (int jt = 0; jt < JT; ++jt) {
-        const int jb = 8 * jt + gid;
-        const int jc = jb < NQ ? jb : NQ - 1;
-        const double sx_ = G[W_TXJ + jc], sy_ = G[w_tyj(N) + jc];
-#pragma unroll
-        for (int s2 = 0; s2 < KT; ++s2) {
-          const int l = 4 * s2 + tig;
-          const double bd = sDt[((jt * KT + s2) << 5) + lane];
-          dmma(vp[jt], Us[(NQ + l) * SP + i], sx_ * bd);
-          dmma(vp[jt], Us[(2 * NQ + l) * SP + i], sy_ * bd);
-          dmma(vp[jt], Us[(3 * NQ + l) * SP + i], tzJ * bd);
-          dmma(pdt[jt], Us[l * SP + i], bd);
-        }
-      }
-    }
+    if (!C::VF) vol_products();
 
     // ---- D: quad faces (jf0 R0_e + jf1 R1_e) [Fp_e | Fu_e] -------------------
     double qp[JT][2], qu[3][JT][2];
