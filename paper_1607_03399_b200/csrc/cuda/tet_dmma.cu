@@ -36,6 +36,10 @@ __host__ __device__ constexpr int cf_stride(int x) {
   return (x % 16 == 4 || x % 16 == 12) ? x : cf_stride(x + 1);
 }
 
+// build the W_a columns between issuing the neighbour gathers and using them
+#ifndef PDG_TET_BV_FIRST
+#define PDG_TET_BV_FIRST 1
+#endif
 constexpr int kTB = 8; // tets per batch (the N dimension of every product)
 // CTA size cap and stage depth: 640 / double-buffered measured best at N = 4
 // (single-buffered 480/640-thread variants spill: 1.92 / 2.13 vs 1.65 ms)
@@ -249,7 +253,25 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
                            ? __ldcs(res_src + p.tet_base + (t0 + t) * 4 * NP + fld * NP + n) : 0.0;
       }
 
+    // the W_a columns of the volume products (P, r/s/t-combinations of the velocity)
+    // measured (profiles/round1_tet_bv_ab.txt): N = 3 -0.9%, N = 5 -0.6%, N = 6 -1.7%, N = 4 +2.5% (spills)
+    constexpr bool kBvFirst = PDG_TET_BV_FIRST && N != 4;
+    auto build_bv = [&]() {
+    if (vol) {
+      for (int m = tt; m < nel * NP; m += 32 * T) {
+        const int t = m / NP, n = m - t * NP;
+        const double* Ut = U + t * C::US;
+        const double* Gt = G + t * kTG;
+        const double ux = Ut[NP + n], uy = Ut[2 * NP + n], uz = Ut[3 * NP + n];
+        BVb[t * VST + n] = Ut[n];
+        BVb[(kTB + t) * VST + n] = Gt[T_RX] * ux + Gt[T_RY] * uy + Gt[T_RZ] * uz;
+        BVb[(2 * kTB + t) * VST + n] = Gt[T_SX] * ux + Gt[T_SY] * uy + Gt[T_SZ] * uz;
+        BVb[(3 * kTB + t) * VST + n] = Gt[T_TX] * ux + Gt[T_TY] * uy + Gt[T_TZ] * uz;
+      }
+    }
+    };
     // ---- fluxes of the batch (scaled by J_f / J) and the W_a columns ------------
+    if (kBvFirst && !surf) build_bv();
     if (surf) {
       // all gathers of this thread's face-node tasks first (independent loads in
       // flight together), then the flux arithmetic
@@ -279,6 +301,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
           }
         }
       }
+      if (kBvFirst) build_bv(); // shared-memory work while the gathers are in flight
 #pragma unroll
       for (int q = 0; q < C::TASKS; ++q) {
         const int m = tt + 32 * T * q;
@@ -309,18 +332,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
         }
       }
     }
-    if (vol) {
-      for (int m = tt; m < nel * NP; m += 32 * T) {
-        const int t = m / NP, n = m - t * NP;
-        const double* Ut = U + t * C::US;
-        const double* Gt = G + t * kTG;
-        const double ux = Ut[NP + n], uy = Ut[2 * NP + n], uz = Ut[3 * NP + n];
-        BVb[t * VST + n] = Ut[n];
-        BVb[(kTB + t) * VST + n] = Gt[T_RX] * ux + Gt[T_RY] * uy + Gt[T_RZ] * uz;
-        BVb[(2 * kTB + t) * VST + n] = Gt[T_SX] * ux + Gt[T_SY] * uy + Gt[T_SZ] * uz;
-        BVb[(3 * kTB + t) * VST + n] = Gt[T_TX] * ux + Gt[T_TY] * uy + Gt[T_TZ] * uz;
-      }
-    }
+    if (!kBvFirst) build_bv();
     team_sync(bar_id, 32 * T);
 
     // ---- row tile w: volume and lift products -------------------------------------
