@@ -82,6 +82,9 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #ifndef PDG_VOL_FIRST
 #define PDG_VOL_FIRST 1
 #endif
+#ifndef PDG_VF_N5
+#define PDG_VF_N5 0
+#endif
 // k permutation of the triangle products (G2/G3) at odd NT: in every block of four
 // k-steps lane (gid, tig) takes k = 16 b + 4 tig + s instead of 4 s + tig, so the
 // B reads {slice * stride + k} (odd stride) and the compact-L A reads {k * NT + i}
@@ -136,7 +139,7 @@ struct DCfg {
   static constexpr bool NOEND = FBUF == 2 && NSTAGE == 2;
   // measured (profiles/round1_volfirst_ab.txt): N = 4 -2.8%, N = 6 -4.5%, N = 7 -6.5%,
   // N = 5 +0.4% (with the dropped end barrier its gathers are already covered)
-  static constexpr bool VF = PDG_VOL_FIRST && N != 5;
+  static constexpr bool VF = PDG_VOL_FIRST && (N != 5 || PDG_VF_N5);
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
   // <= PDG_THREAD_CAP threads per CTA: 384 keeps >= 168 registers per thread
   // (profiles/round1_compact_ops_ab.txt: compact operators + 384 beat 512)
