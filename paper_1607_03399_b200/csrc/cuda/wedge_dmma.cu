@@ -158,7 +158,9 @@ inline int ticket_batch(int N) {
     return v ? std::atoi(v) : 0;
   }();
   if (env > 0) return env;
-  return N <= 3 ? 8 : 2; // measured sweep, round 1 (profiles/round1_ticket_batch.txt)
+  // measured sweeps, round 1 (profiles/round1_ticket_batch.txt; after the schedule
+  // changes N = 4 prefers 4: profiles/round1_ticket_batch2.txt)
+  return N <= 3 ? 8 : (N == 4 ? 4 : 2);
 }
 
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
