@@ -134,7 +134,8 @@ inline int ticket_batch(int N) {
     return v ? std::atoi(v) : 0;
   }();
   if (env > 0) return env;
-  return N <= 3 ? 8 : 2; // measured sweep, round 1 (profiles/round1_ticket_batch.txt)
+  // measured sweeps, round 1 (profiles/round1_ticket_batch.txt, round1_ticket_batch2.txt)
+  return N <= 3 ? 8 : 4;
 }
 
 /// big WADG tables in L1-cached global memory instead of shared memory
