@@ -18,8 +18,17 @@ C ABI with host buffers: per step H2D of the state from pinned memory,
 pdg_step_lserk, D2H of the state.
 
 --impl reference: the reference's CPU algorithm (the oracle port in oracle/,
-because the reference itself cannot be built here) on the box's host cores,
-on a bounded sample (same surface, fewer sublayers).
+because the reference itself cannot be built here: Eigen3 is absent) on the
+box's host cores, on a bounded sample (same surface, fewer sublayers).  That
+process never loads the product library: the oracle carries its own copy of
+the host setup code and is rebuilt on the box with the reference's
+-O3 -march=native (proj/CMakeLists.txt:10).
+
+--gpus N without torchrun: bench.py re-launches itself under
+torch.distributed.run with N ranks (one per GPU; it refuses to run when fewer
+than N GPUs are visible).  --scaling weak (default, config 5 weak: 1e6 owned
+wedges per GPU) or strong (config 5 strong: the n=200 x 50-sublayer mesh,
+4e6 wedges, split over the N GPUs).
 """
 from __future__ import annotations
 
@@ -143,27 +152,62 @@ def dist_env():
     return ws, rank, local
 
 
-def cpu_sample(degree, threads, target_s=15.0, parallel_update=False, surface_n=100, sublayers=(1, 1, 1)):
-    """Oracle (reference algorithm) DOF-updates/s on a bounded sample of the workload."""
-    import numpy as np
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def native_oracle(timeout_s=300):
+    """Build the oracle with the reference's -O3 -march=native on THIS host
+    (oracle/build_native); fall back to the portable prebuilt oracle."""
+    jobs = str(os.cpu_count() or 1)
+    cmd = ["make", "-s", "-C", os.path.join(ROOT, "oracle"), "-j", jobs, "OUT=build_native", "HOST_ARCH=-march=native",
+           "build_native/liboracle.so"]
+    try:
+        r = subprocess.run(cmd, capture_output=True, timeout=timeout_s)
+        lib = os.path.join(ROOT, "oracle", "build_native", "liboracle.so")
+        if r.returncode == 0 and os.path.exists(lib):
+            return lib, "-O3 -march=native -fopenmp (built on this host)"
+    except Exception:
+        pass
+    return os.path.join(ROOT, "oracle", "build", "liboracle.so"), "-O3 -march=x86-64-v3 -fopenmp (prebuilt, portable)"
+
+
+def cpu_sample(degree, threads, steps, warmup=1, surface_n=100, sublayers=(1, 1, 1), oracle_lib=None):
+    """The reference's CPU algorithm (oracle port, solver.cpp:536-557) on a bounded
+    sample of the workload, timed per LSERK45 step in both update variants:
+    'faithful' = the reference's serial update loop (solver.cpp:546-549),
+    'parallel' = OpenMP on the update as well (a fair best-effort CPU).
+    Loads only liboracle.so (its own mesh/discretization build), never the product."""
+    if oracle_lib:
+        os.environ["PDG_ORACLE_LIB"] = oracle_lib
     import oracle_binding as ob
-    import paper_1607_03399_b200 as pdg
-    mesh = layered_workload(surface_n, list(sublayers))
-    d = pdg.build_discretization(mesh, degree, threads=threads)
-    s = pdg.make_initial_state(d, "gaussian", [0.25, 0.0, 0.0, 0.0])
-    dt = pdg.estimate_dt(d, 0.5)
-    u = ob.lserk(d, s.u, dt, 1, threads, parallel_update)  # warm-up step
-    steps, elapsed = 0, 0.0
-    while elapsed < target_s and steps < 1000:
-        t0 = time.perf_counter()
-        u = ob.lserk(d, u, dt, 1, threads, parallel_update)
-        elapsed += time.perf_counter() - t0
-        steps += 1
-    rate = d.total_dofs * steps / elapsed
-    sample = (f"oracle port of solver.cpp:536-557 ({'parallel' if parallel_update else 'serial'} update), "
-              f"{mesh.num_wedges()} wedges (surface n={surface_n}, sublayers {list(sublayers)}), N={degree}, "
-              f"{steps} steps in {elapsed:.1f}s")
-    return rate, sample
+    t0 = time.perf_counter()
+    d = ob.layered_disc(surface_n, [-1.0, -0.4, 0.2, 1.0], list(sublayers), [(1.0, 1.0), (1.0, 4.0), (1.0, 2.25)],
+                        degree, threads=threads)
+    u0 = d.gaussian(0.25)
+    dt = d.estimate_dt(0.5)
+    setup = time.perf_counter() - t0
+    rates = {"faithful": [], "parallel": []}
+    u = u0
+    for it in range(warmup + steps):
+        for kind in ("parallel", "faithful"):
+            t1 = time.perf_counter()
+            u = ob.lserk(d, u, dt, 1, threads, kind == "parallel")
+            el = time.perf_counter() - t1
+            if it >= warmup:
+                rates[kind].append(d.total_dofs / el)
+    med = {k: (sorted(v)[len(v) // 2] if v else 0.0) for k, v in rates.items()}
+    sample = (f"oracle port of solver.cpp:536-557 on {d.num_wedges} wedges (surface n={surface_n}, sublayers "
+              f"{list(sublayers)}; the GPU arm runs 1e6), N={degree}, {d.total_dofs} DOFs, median of {steps} timed "
+              f"LSERK45 steps per variant after {warmup} warm-up, {threads} OpenMP threads, setup {setup:.1f}s")
+    return med, sample, d.total_dofs
 
 
 def run_reference_arm(args):
@@ -171,20 +215,22 @@ def run_reference_arm(args):
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    rates = []
-    sample = ""
-    for it in range(args.warmup + args.steps):
-        rate, sample = cpu_sample(args.degree, threads, target_s=args.ref_seconds, parallel_update=False,
-                                  sublayers=(1, 1, 1))
-        if it >= args.warmup:
-            rates.append(rate)
-    value = sorted(rates)[len(rates) // 2] if rates else 0.0
+    lib, build = native_oracle()
+    med, sample, _ = cpu_sample(args.degree, threads, steps=args.steps, warmup=args.warmup, oracle_lib=lib)
+    value = med["parallel"]
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (gaussian pulse on generated layered wedge mesh)",
-        "config": {"workload": "configs[1] layered wedges, bounded CPU sample", "degree": args.degree},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": max(ws, args.gpus),
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (gaussian pulse on generated layered wedge mesh)",
+        "config": {"workload": "configs[1] layered wedges (n=100 surface), bounded CPU sample of 3 sublayers",
+                   "degree": args.degree, "same_config": False,
+                   "why_not_same": "one reference LSERK step on the 1e6-wedge mesh takes ~13 s on 16 cores; the "
+                                   "per-DOF rate of the 60k-wedge sample (state 0.24 GB at N=5, far beyond the "
+                                   "CPU caches) is the same algorithm on the same element types"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                         "variant": "parallel update (value); faithful serial update below",
+                         "faithful_serial_update": med["faithful"], "build": build, "cpu": cpu_model()},
+        "variants": {"parallel_update": med["parallel"], "faithful_serial_update": med["faithful"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -301,9 +347,11 @@ def measure_degree(args, degree, ws, rank, local, peaks, with_e2e=True):
 
 
 def measure_degree_dist(args, degree, ws, rank, local, peaks):
-    """N > 1: weak scaling, rank r owns the r-th slab of 1e6 wedges (stack of ws copies of
-    the config-2 slab, config 5); ghosts are one sublayer above and below and are
-    refreshed with NCCL point-to-point before every LSERK stage."""
+    """N > 1 (config 5).  Weak: rank r owns the r-th slab of 1e6 wedges (stack of
+    ws copies of the config-2 slab).  Strong: the n=200 x 50-sublayer mesh (4e6
+    wedges) with its sublayers split over the ranks.  Ghosts are one sublayer
+    above and below; their face traces are refreshed with NCCL point-to-point
+    before every LSERK stage, overlapped with the interior elements."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -312,8 +360,11 @@ def measure_degree_dist(args, degree, ws, rank, local, peaks):
     from paper_1607_03399_b200.distributed import DistributedLSERK
 
     t_setup = time.perf_counter()
-    part = P.layered_slab(args.surface_n, [-1.0, -0.4, 0.2, 1.0], args.sublayers,
-                          [(1.0, 1.0), (1.0, 4.0), (1.0, 2.25)], ws, rank)
+    media = [(1.0, 1.0), (1.0, 4.0), (1.0, 2.25)]
+    if args.scaling == "strong":
+        part = P.layered_strong(args.strong_n, [-1.0, -0.4, 0.2, 1.0], args.sublayers, media, ws, rank)
+    else:
+        part = P.layered_slab(args.surface_n, [-1.0, -0.4, 0.2, 1.0], args.sublayers, media, ws, rank)
     solver = DistributedLSERK(part, degree, device=local, threads=os.cpu_count() or 1, flags=pdg.capi.CTX_TIMING)
     d = solver.disc
     s = pdg.make_initial_state(d, "gaussian", [0.25, 0.0, 0.0, 0.0])
@@ -342,6 +393,8 @@ def measure_degree_dist(args, degree, ws, rank, local, peaks):
     tot = torch.tensor([owned_dofs], dtype=torch.float64, device="cuda")
     dist.all_reduce(tot)
     value = float(tot.item()) * args.steps / (ms / 1e3)
+    total_wedges = torch.tensor([part.n_owned], dtype=torch.float64, device="cuda")
+    dist.all_reduce(total_wedges)
     # roofline of this rank's wedge stage kernel: a stage is an interior and a boundary
     # launch over disjoint owned elements, so per-stage time = summed launch time / stages
     kt = solver.kernel_times(reset=True)
@@ -375,12 +428,34 @@ def measure_degree_dist(args, degree, ws, rank, local, peaks):
     parts_nonempty = int(interior > 0) + int(owned - interior > 0)
     solver.close()
     return {"degree": degree, "value": value, "ms_per_step": ms / args.steps, "total_dofs": owned_dofs,
+            "total_wedges": int(total_wedges.item()),
             "wedges": part.n_owned, "setup_s": round(setup_s, 1), "clocks": clk.summary(),
             "roofline": roof, "e2e": e2e, "wedge_kernel_avg_ms": stage_ms,
             # per stage: the non-empty interior / boundary stage launches, one trace gather
             # and one trace scatter per peer
             "gpu_launches": args.steps * 5 * (parts_nonempty + 2 * len(solver.peers)),
             "exchange_bytes_per_stage": solver.exchange_bytes}
+
+
+def relaunch(args):
+    """--gpus N outside torchrun: start N ranks (one per GPU) under
+    torch.distributed.run with the same arguments; refuse when fewer than N
+    GPUs are visible (NCCL cannot put two ranks on one device)."""
+    import socket
+    if args.impl == "ours":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}; "
+                  f"refusing to report a {have}-GPU number as {args.gpus}", file=sys.stderr, flush=True)
+            return 3
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -393,9 +468,11 @@ def main():
     ap.add_argument("--degrees", default="1,2,3,4,6,7",
                     help="comma list for the order sweep reported under 'sweep' ('' = headline degree only)")
     ap.add_argument("--surface-n", type=int, default=100)
+    ap.add_argument("--strong-n", type=int, default=200, help="surface n of the strong-scaling mesh (x 50 sublayers)")
     ap.add_argument("--sublayers", default="15,15,20")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--ref-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-steps", type=int, default=3, help="timed CPU-baseline LSERK steps per update variant")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="layered", choices=["layered", "hybrid"],
                     help="layered = configs[1] (1e6 wedges); hybrid = configs[2] (wedge layers over a tet cap)")
@@ -408,33 +485,46 @@ def main():
     args.sublayers = [int(x) for x in args.sublayers.split(",")]
     args.warmup = max(3, args.warmup)
 
+    ws, rank, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        return relaunch(args)
+    if "WORLD_SIZE" in os.environ and ws != args.gpus and args.gpus > 1:
+        print(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}", file=sys.stderr, flush=True)
+        return 3
     if args.impl == "reference":
         return run_reference_arm(args)
 
-    ws, rank, local = dist_env()
     import torch
     torch.cuda.set_device(local)
-    use_dist = ws > 1 or args.partitioned
+    use_dist = ws > 1 or args.partitioned or args.scaling == "strong"
     if use_dist:
         if ws == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29561")
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
+        # communicator setup lines (rank count, NVLS / P2P transport) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks = load_peaks()
     if use_dist:
         head = measure_degree_dist(args, args.degree, ws, rank, local, peaks)
         if rank == 0:
+            if args.scaling == "strong":
+                wl = (f"configs[4] strong: layered wedge mesh n={args.strong_n} surface x {sum(args.sublayers)} "
+                      f"sublayers ({head['total_wedges']} wedges in total, fixed), sublayers split over {ws} GPU(s)")
+            else:
+                wl = ("configs[4] weak: layered wedge slabs, 1e6 owned wedges per GPU stacked in z")
             line = {
                 "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (gaussian pulse on generated layered wedge mesh)",
-                "config": {"workload": "configs[4]: layered wedge slabs, 1e6 owned wedges per GPU stacked in z, "
-                                       "face traces of the one-sublayer ghost layer exchanged per LSERK stage (NCCL p2p) "
-                                       "on a side stream, overlapped with the interior elements",
+                "config": {"workload": wl + ", face traces of the one-sublayer ghost layer exchanged per LSERK "
+                                            "stage (NCCL p2p) on a side stream, overlapped with the interior elements",
                            "degree": args.degree, "wedges_per_gpu": head["wedges"],
+                           "total_wedges": head["total_wedges"],
                            "parallelism": f"mesh partition x{ws}", "l2": "inputs larger than L2, no flush",
                            "exchange_bytes_per_stage_per_rank": head["exchange_bytes_per_stage"]},
                 "roofline": head["roofline"], "cpu_baseline": None, "e2e": head["e2e"],
@@ -451,12 +541,16 @@ def main():
             continue
         r = measure_degree(args, deg, ws, rank, local, peaks, with_e2e=False)
         sweep.append({k: r[k] for k in ("degree", "value", "ms_per_step", "wedge_kernel_avg_ms", "roofline",
-                                        "total_dofs", "setup_s", "gpu_launches", "tensor_roofline") if k in r})
+                                        "total_dofs", "setup_s", "gpu_launches", "tensor_roofline",
+                                        "tet_kernel_avg_ms", "tet_roofline") if k in r})
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        rate, sample = cpu_sample(args.degree, threads, target_s=12.0, parallel_update=False, sublayers=(1, 1, 1))
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
+        med, sample, _ = cpu_sample(args.degree, threads, steps=args.cpu_steps, warmup=1)
+        cpu = {"value": med["parallel"], "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+               "variant": "parallel update (value)", "faithful_serial_update": med["faithful"],
+               "build": "-O3 -march=x86-64-v3 -fopenmp (prebuilt oracle; bench.py --impl reference rebuilds it "
+                        "with -march=native)", "cpu": cpu_model()}
     if rank == 0:
         line = {
             "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -471,7 +565,7 @@ def main():
                                    "weight-adjusted (WADG) mass, no per-wedge operator storage") + ", upwind",
                        "mass": args.mass,
                        "degree": args.degree, "wedges_per_gpu": head["wedges"], "total_dofs_per_gpu": head["total_dofs"],
-                       "parallelism": f"mesh partition x{ws}" if ws > 1 else "single GPU",
+                       "parallelism": "single GPU",
                        "l2": "inputs larger than L2 (state >> 126 MB), no flush"},
             "roofline": head["roofline"], "cpu_baseline": cpu, "e2e": head.get("e2e"),
             "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
@@ -483,8 +577,6 @@ def main():
         if sweep:
             line["sweep"] = sweep
         print(json.dumps(line), flush=True)
-    if ws > 1:
-        torch.distributed.destroy_process_group()
     return 0
 
 

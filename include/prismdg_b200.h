@@ -175,6 +175,11 @@ int pdg_kernel_times(pdg_ctx* ctx, double* wedge_ms, int64_t* wedge_launches, do
                      int64_t* tet_launches, int reset);
 /* algorithmic bytes moved per launch of the wedge / tet stage kernels */
 int pdg_stage_bytes(pdg_ctx* ctx, double* wedge_bytes, double* tet_bytes);
+/* the most recent wedge (out[0..3]) and tet (out[4..7]) stage launch:
+ * {launched (0: empty element range, nothing launched), work teams started,
+ *  tickets (work units handed out by the global work counter), elements per
+ *  ticket}.  tickets / teams > 1 means teams loop over several work units. */
+int pdg_launch_info(pdg_ctx* ctx, int64_t out[8]);
 /* number of device elements and the device element -> reference element map */
 int pdg_device_order(pdg_ctx* ctx, int64_t* dev_to_ref);
 
@@ -255,7 +260,12 @@ typedef struct {
 
 /* run_simulation (solver.hpp:148-149) on the device; u_inout/time_inout hold
  * the SolutionState (reference layout, host).  energy_log (may be NULL) gets
- * up to max_log (time, energy) pairs. */
+ * up to max_log (time, energy) pairs.  When the watchdog fails
+ * (PDG_ERR_NUMERICAL) u_inout / time_inout hold the state at the failure time,
+ * as the reference's SolutionState does.  Difference from the reference: the
+ * AB3 history is not part of the host state, so every call starts a fresh
+ * history (two LSERK45 bootstrap steps); the reference resumes the history
+ * kept in SolutionState::history (solver.hpp:84-90) across runs. */
 int pdg_run_simulation(pdg_ctx* ctx, double* u_inout, double* time_inout,
                        const pdg_run_options* opts, pdg_run_result* result, double* energy_log,
                        int max_log);

@@ -30,12 +30,14 @@ struct Block {
   double operator()(int j, int i) const { return v[(std::size_t)i * nq + j]; }
 };
 
+// per-thread workspace, allocated once per compute_rhs call like the
+// reference's thread_local workspace (solver.cpp:26-44)
 struct Scratch {
-  Block dr, ds, dt, w;
-  std::vector<double> fp, fu, lift_u, va, vb, vc;
+  Block dr, ds, dt, w, tmp, rp;
+  std::vector<double> fp, fu, lift_u, va, vb, vc, vd, tv;
   Scratch(int nq, int nt, int max_np, int max_nfp)
-      : dr(nq, nt), ds(nq, nt), dt(nq, nt), w(nq, nt), fp(max_nfp), fu(max_nfp), lift_u(max_np), va(max_np),
-        vb(max_np), vc(max_np) {}
+      : dr(nq, nt), ds(nq, nt), dt(nq, nt), w(nq, nt), tmp(nq, nt), rp(nq, nt), fp(max_nfp), fu(max_nfp),
+        lift_u(max_np), va(max_np), vb(max_np), vc(max_np), vd(max_np), tv(nt) {}
 };
 
 // out(j,i) = sum_k X(j,k) M(i,k)   ("X * M^T")
@@ -89,7 +91,7 @@ void wedge_volume_elem(const Discretization& d, int e, const double* u, double* 
   double* RUX = rhs + base + np;
   double* RUY = rhs + base + 2 * np;
   double* RUZ = rhs + base + 3 * np;
-  Block tmp(nq, nt);
+  Block& tmp = ws.tmp;
 
   // pressure gradient
   times_transpose(P, nq, nt, refs.tri.dr, ws.dr);
@@ -110,7 +112,7 @@ void wedge_volume_elem(const Discretization& d, int e, const double* u, double* 
     for (int j = 0; j < nq; ++j) RUZ[i * nq + j] = -g.tzJ * tmp(j, i);
 
   // velocity divergence with one folded lift application
-  Block rp(nq, nt);
+  Block& rp = ws.rp;
   times_transpose(UX, nq, nt, refs.tri.dr, ws.dr);
   times_transpose(UX, nq, nt, refs.tri.ds, ws.ds);
   for (int i = 0; i < nt; ++i)
@@ -158,7 +160,8 @@ void tet_volume_elem(const Discretization& d, int e, const double* u, double* rh
     rhs[base + 2 * np + n] = -(g.ry * a[n] + g.sy * b[n] + g.ty * c[n]);
     rhs[base + 3 * np + n] = -(g.rz * a[n] + g.sz * b[n] + g.tz * c[n]);
   }
-  std::vector<double> rp(np, 0.0);
+  double* rp = ws.vd.data();
+  std::fill(rp, rp + np, 0.0);
   const double* comps[3] = {u + base + np, u + base + 2 * np, u + base + 3 * np};
   const double cr[3] = {g.rx, g.ry, g.rz}, cs[3] = {g.sx, g.sy, g.sz}, ct[3] = {g.tx, g.ty, g.tz};
   for (int q = 0; q < 3; ++q) {
@@ -214,7 +217,7 @@ void surface_elem(const Discretization& d, int e, const double* u, double* rhs, 
         const Vec& prof = exact ? (bottom ? refs.line.lift_bottom : refs.line.lift_top)
                                 : (bottom ? refs.line.lumped_lift_bottom : refs.line.lumped_lift_top);
         const double jf = bottom ? d.wgeo[e].jf_bottom : d.wgeo[e].jf_top;
-        std::vector<double> tmp(nt);
+        double* tmp = ws.tv.data();
         for (int i = 0; i < nt; ++i) {
           double s = 0.0;
           for (int k = 0; k < nt; ++k) s += Lik(d, e, i, k) * ws.fp[k];

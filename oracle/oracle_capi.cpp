@@ -1,12 +1,16 @@
 // CPU ORACLE (test infrastructure only; see oracle.hpp): C entry points used by
-// tests/ (ctypes) and bench.py's CPU baseline.  Handles are the product's
-// pdg_disc (a prismdg::Discretization*), built by include/prismdg_b200.h.
+// tests/ (ctypes) and bench.py's CPU baseline.  Handles are a
+// prismdg::Discretization*: either the product's pdg_disc (tests check the
+// device path against the oracle on the very same Discretization) or one the
+// oracle builds itself with orc_disc_stack_layers (bench.py's CPU arm, which
+// must not load the product library).
 #include <chrono>
 #include <cstdint>
 #include <exception>
 #include <string>
 
 #include "oracle.hpp"
+#include "prismdg/solver.hpp"
 
 using prismdg::Discretization;
 
@@ -78,6 +82,56 @@ int orc_run(const void* disc, double* u, double* time, double final_time, double
     out[6] = r.stable ? 1.0 : 0.0;
   });
 }
+
+/// the oracle's own Discretization of a stack_layers mesh (mesh.hpp:59-68;
+/// the reference's "layers" config kind, config.cpp:232-243 + 152-178): xy[nv][2],
+/// tris[ntri][3], z_bottom/z_top[nlayers][nv], sublayers[nlayers],
+/// media[nlayers][2] = {rho, kappa}; exact mass, upwind flux
+int orc_disc_stack_layers(int nv, const double* xy, int ntri, const int* tris, int nlayers, const double* z_bottom,
+                          const double* z_top, const int* sublayers, const double* media, int degree, int threads,
+                          void** out) {
+  return guard([&] {
+    std::vector<std::array<double, 2>> pts(nv);
+    for (int v = 0; v < nv; ++v) pts[v] = {xy[2 * v], xy[2 * v + 1]};
+    std::vector<std::array<int, 3>> tr(ntri);
+    for (int t = 0; t < ntri; ++t) tr[t] = {tris[3 * t], tris[3 * t + 1], tris[3 * t + 2]};
+    std::vector<prismdg::LayerSpec> layers(nlayers);
+    for (int l = 0; l < nlayers; ++l) {
+      layers[l].z_bottom.assign(z_bottom + (std::size_t)l * nv, z_bottom + (std::size_t)(l + 1) * nv);
+      layers[l].z_top.assign(z_top + (std::size_t)l * nv, z_top + (std::size_t)(l + 1) * nv);
+      layers[l].sublayers = sublayers[l];
+      layers[l].media.rho = media[2 * l];
+      layers[l].media.kappa = media[2 * l + 1];
+    }
+    auto* d = new Discretization(prismdg::build_discretization(prismdg::stack_layers(pts, tr, layers), degree, {},
+                                                               prismdg::QuadratureMode::exact, threads));
+    *out = d;
+  });
+}
+
+/// {total_dofs, num_wedges, num_tets}
+int orc_disc_counts(const void* disc, long long* out) {
+  return guard([&] {
+    out[0] = (long long)D(disc)->total_dofs;
+    out[1] = D(disc)->mesh.num_wedges();
+    out[2] = D(disc)->mesh.num_tets();
+  });
+}
+
+/// make_initial_state(gaussian_pulse(width, {cx, cy, cz})) (solver.cpp:469-502)
+int orc_disc_gaussian(const void* disc, double width, double cx, double cy, double cz, double* u) {
+  return guard([&] {
+    const auto s = prismdg::make_initial_state(*D(disc), prismdg::gaussian_pulse(width, {cx, cy, cz}));
+    std::copy(s.u.begin(), s.u.end(), u);
+  });
+}
+
+/// estimate_dt (solver.cpp:437-447)
+int orc_disc_estimate_dt(const void* disc, double cfl, double* dt) {
+  return guard([&] { *dt = prismdg::estimate_dt(*D(disc), cfl); });
+}
+
+void orc_disc_free(void* disc) { delete static_cast<Discretization*>(disc); }
 
 int orc_gll_newton(int npts, double* x, double* w) {
   return guard([&] {

@@ -146,6 +146,7 @@ SIGNATURES = {
     "pdg_kernel_times": (C.c_int, [P, DP, I64P, DP, I64P, C.c_int]),
     "pdg_stage_bytes": (C.c_int, [P, DP, DP]),
     "pdg_device_order": (C.c_int, [P, I64P]),
+    "pdg_launch_info": (C.c_int, [P, I64P]),
     "pdg_run_simulation": (C.c_int, [P, DP, DP, C.POINTER(RunOptions), C.POINTER(RunResult), DP, C.c_int]),
     "pdg_create_partitioned": (C.c_int, [P, C.c_int, C.c_int, C.POINTER(C.c_ubyte), PP]),
     "pdg_active_counts": (C.c_int, [P, I64P]),

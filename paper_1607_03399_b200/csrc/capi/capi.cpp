@@ -579,6 +579,20 @@ int pdg_stage_bytes(pdg_ctx* ctx, double* wedge_bytes, double* tet_bytes) {
   });
 }
 
+int pdg_launch_info(pdg_ctx* ctx, int64_t out[8]) {
+  return guarded([&] {
+    need(ctx, "context");
+    need(out, "output");
+    for (int k = 0; k < 2; ++k) {
+      const auto& li = ctx->last_launch[k];
+      out[4 * k] = li.launched;
+      out[4 * k + 1] = li.teams;
+      out[4 * k + 2] = li.tickets;
+      out[4 * k + 3] = li.per_ticket;
+    }
+  });
+}
+
 int pdg_device_order(pdg_ctx* ctx, int64_t* dev_to_ref) {
   return guarded([&] {
     need(ctx, "context");
@@ -628,6 +642,23 @@ int pdg_run_simulation(pdg_ctx* ctx, double* u_inout, double* time_inout, const 
       snaps.take(t);
       next_snapshot_t += opts->snapshot_interval;
     }
+    // the reference leaves SolutionState at the failure time when the
+    // watchdog throws (solver.cpp:647-661): hand the device state back first
+    struct StateOnThrow {
+      pdg_ctx* c;
+      double* u;
+      double* time;
+      const double* t;
+      bool armed = true;
+      ~StateOnThrow() {
+        if (!armed) return;
+        try {
+          pdg::get_state(c, u, false);
+          *time = *t;
+        } catch (...) {
+        }
+      }
+    } on_throw{ctx, u_inout, time_inout, &t};
     for (int n = 0; n < steps; ++n) {
       if (ab3)
         pdg::step_ab3(ctx, dt, 1);
@@ -659,6 +690,7 @@ int pdg_run_simulation(pdg_ctx* ctx, double* u_inout, double* time_inout, const 
     res.final_time = t;
     res.final_energy = pdg::energy(ctx);
     res.num_logged = nlog;
+    on_throw.armed = false;
     pdg::get_state(ctx, u_inout, false);
     *time_inout = t;
     *result = res;

@@ -156,16 +156,19 @@ __global__ void reduce_sum_kernel(const double* __restrict__ in, int n, double* 
 }
 
 template <int N>
-__global__ void check_finite_kernel(long long Kw, long long Kt, const double* __restrict__ u,
+__global__ void check_finite_kernel(long long Kw, long long Kw_act, long long Kt_act, const double* __restrict__ u,
                                     const int* __restrict__ dev_to_ref,
                                     unsigned long long* first_bad) {
+  // owned elements only: wedges [0, Kw_act), tets [Kw, Kw + Kt_act) (ghosts follow
+  // the owned elements of their kind and belong to another rank)
   constexpr int NPW = npd_of(N), NPT = npt_of(N); // device wedge block (padding entries are zero)
-  const long long wdofs = Kw * 4 * NPW;
-  const long long total = wdofs + Kt * 4 * NPT;
+  const long long wact = Kw_act * 4 * NPW, wall = Kw * 4 * NPW;
+  const long long total = wact + Kt_act * 4 * NPT;
   for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
-    if (!isfinite(u[idx])) {
-      const long long d = idx < wdofs ? idx / (4 * NPW) : Kw + (idx - wdofs) / (4 * NPT);
+    const long long at = idx < wact ? idx : wall + (idx - wact);
+    if (!isfinite(u[at])) {
+      const long long d = idx < wact ? idx / (4 * NPW) : Kw + (idx - wact) / (4 * NPT);
       atomicMin(first_bad, (unsigned long long)dev_to_ref[d]);
     }
   }
@@ -309,12 +312,13 @@ cudaError_t launch_unpack_states(int N, long long Kw, const long long* dev_elems
   return cudaGetLastError();
 }
 
-cudaError_t launch_check_finite(int N, long long Kw, long long Kt, const double* u,
+cudaError_t launch_check_finite(int N, long long Kw, long long Kw_act, long long Kt_act, const double* u,
                                 const int* dev_to_ref, unsigned long long* first_bad,
                                 cudaStream_t s) {
-  const long long total = Kw * 4 * npd_of(N) + Kt * 4 * npt_of(N);
+  const long long total = Kw_act * 4 * npd_of(N) + Kt_act * 4 * npt_of(N);
   if (total == 0) return cudaSuccess;
-  PDG_DISPATCH(N, (check_finite_kernel<NN><<<grid_for(total, 256), 256, 0, s>>>(Kw, Kt, u, dev_to_ref, first_bad)));
+  PDG_DISPATCH(N, (check_finite_kernel<NN><<<grid_for(total, 256), 256, 0, s>>>(Kw, Kw_act, Kt_act, u, dev_to_ref,
+                                                                                   first_bad)));
   return cudaGetLastError();
 }
 

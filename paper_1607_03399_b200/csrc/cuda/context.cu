@@ -131,22 +131,35 @@ int dev_node_of(const prismdg::Discretization& d, bool wedge, int nref) {
   return j * nts_of(d.degree) + i; // device slice stride (padded at N = 5)
 }
 
-void launch_checked(pdg_ctx* c, const StageParams& p, bool wedge) {
+void launch_checked(pdg_ctx* c, const StageParams& p0, bool wedge) {
   cudaEvent_t a = nullptr, b = nullptr;
   if (c->flags & 2) {
     PDG_CK(cudaEventCreate(&a));
     PDG_CK(cudaEventCreate(&b));
     PDG_CK(cudaEventRecord(a, c->stream));
   }
+  LaunchInfo info;
+  StageParams p = p0;
+  p.info = &info;
   cudaError_t err = !wedge ? launch_tet_stage(c->N, p, c->stream)
                     : c->wadg ? (c->N <= wedge_wadg_simt_max_degree() ? launch_wedge_wadg_simt_stage(c->N, p, c->stream)
                                                                      : launch_wedge_wadg_stage(c->N, p, c->stream))
                     : c->wedge_simt ? launch_wedge_simt_stage(c->N, p, c->stream)
                                     : launch_wedge_stage(c->N, p, c->stream);
-  if (err != cudaSuccess) throw DeviceError(std::string("stage kernel launch failed: ") + cudaGetErrorString(err));
+  if (err != cudaSuccess) {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+    throw DeviceError(std::string("stage kernel launch failed: ") + cudaGetErrorString(err));
+  }
+  c->last_launch[wedge ? 0 : 1] = info;
   if (c->flags & 2) {
-    PDG_CK(cudaEventRecord(b, c->stream));
-    c->pending.push_back({a, b, wedge ? 0 : 1});
+    if (info.launched) {
+      PDG_CK(cudaEventRecord(b, c->stream));
+      c->pending.push_back({a, b, wedge ? 0 : 1});
+    } else { // an empty element range launches nothing: neither timed nor counted
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
   }
 }
 
@@ -603,6 +616,16 @@ void get_state(pdg_ctx* c, double* u, bool on_device) {
   PDG_CK(cudaStreamSynchronize(c->stream));
 }
 
+// whole-domain entry points read every neighbour's current state; on a
+// partitioned context the ghosts' states are only valid right after the
+// caller's exchange, which only the per-stage entry (stage_lserk) is told about
+static void require_unpartitioned(const pdg_ctx* c, const char* what) {
+  if (c->Kw_act != c->Kw || c->Kt_act != c->Kt)
+    throw prismdg::ConfigError(std::string(what) +
+                               " on a partitioned context would read stale ghost states; step it stage by stage "
+                               "(pdg_step_stage / pdg_step_stage_part) with a ghost exchange before each stage");
+}
+
 static void ensure_rhs(pdg_ctx* c) {
   if (!c->rhs) {
     c->rhs = dalloc<double>((std::size_t)c->dev_dofs);
@@ -612,6 +635,7 @@ static void ensure_rhs(pdg_ctx* c) {
 
 void run_phase(pdg_ctx* c, bool wedge, bool volume) {
   PDG_CK(cudaSetDevice(c->device));
+  require_unpartitioned(c, "a phase function");
   ensure_rhs(c);
   StageParams p = base_params(c);
   p.u_in = c->u[c->cur];
@@ -622,6 +646,7 @@ void run_phase(pdg_ctx* c, bool wedge, bool volume) {
 
 void compute_rhs(pdg_ctx* c, const double* u, double* rhs, bool on_device) {
   PDG_CK(cudaSetDevice(c->device));
+  require_unpartitioned(c, "compute_rhs");
   ensure_rhs(c);
   const std::size_t bytes = (std::size_t)c->total_dofs * 8;
   const double* src = u;
@@ -655,6 +680,7 @@ void get_rhs(pdg_ctx* c, double* rhs, bool on_device) {
 
 void step_lserk(pdg_ctx* c, double dt, int nsteps) {
   PDG_CK(cudaSetDevice(c->device));
+  require_unpartitioned(c, "a whole LSERK step");
   StageParams p = base_params(c);
   p.res = c->res;
   p.dt = dt;
@@ -685,8 +711,7 @@ static void rhs_into(pdg_ctx* c, double* dst) {
 
 void step_ab3(pdg_ctx* c, double dt, int nsteps) {
   PDG_CK(cudaSetDevice(c->device));
-  if (c->Kw_act != c->Kw || c->Kt_act != c->Kt)
-    throw prismdg::ConfigError("AB3 on a partitioned context is not supported");
+  require_unpartitioned(c, "AB3");
   const std::size_t nd = (std::size_t)c->dev_dofs;
   for (auto& h : c->fh)
     if (!h) {
@@ -794,6 +819,7 @@ void assemble_operator(pdg_ctx* c, double* A) {
   // their neighbours: probes in elements at face-graph distance > 2 share one
   // rhs evaluation exactly (the per-row arithmetic is unchanged).  Greedy
   // distance-2 colouring in element order; 4*max(Np) evaluations per colour.
+  require_unpartitioned(c, "operator assembly");
   const prismdg::Discretization& d = *c->disc;
   const int ne = d.num_elements();
   const std::size_t n = d.total_dofs;
@@ -957,7 +983,7 @@ long long check_finite(pdg_ctx* c) {
   PDG_CK(cudaSetDevice(c->device));
   const unsigned long long none = std::numeric_limits<unsigned long long>::max();
   PDG_CK(cudaMemcpyAsync(c->badflag, &none, 8, cudaMemcpyHostToDevice, c->stream));
-  PDG_CK(launch_check_finite(c->N, c->Kw, c->Kt, c->u[c->cur], c->dev_to_ref, c->badflag, c->stream));
+  PDG_CK(launch_check_finite(c->N, c->Kw, c->Kw_act, c->Kt_act, c->u[c->cur], c->dev_to_ref, c->badflag, c->stream));
   unsigned long long r = none;
   PDG_CK(cudaMemcpyAsync(&r, c->badflag, 8, cudaMemcpyDeviceToHost, c->stream));
   PDG_CK(cudaStreamSynchronize(c->stream));

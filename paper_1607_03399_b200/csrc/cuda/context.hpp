@@ -71,6 +71,8 @@ struct pdg_ctx {
   double wedge_ms = 0.0, tet_ms = 0.0;
   long long wedge_launches = 0, tet_launches = 0;
 
+  pdg::LaunchInfo last_launch[2]; // most recent wedge / tet stage launch
+
   double wedge_bytes_first = 0.0, wedge_bytes_later = 0.0;
   double tet_bytes_first = 0.0, tet_bytes_later = 0.0;
   long long stage_launches_first = 0, stage_launches_later = 0;

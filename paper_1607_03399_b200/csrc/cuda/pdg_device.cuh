@@ -100,6 +100,16 @@ enum : int {
   M_FIRST = 32,    // a == 0: do not read res
 };
 
+/// what a stage launcher did (host side, filled by every launcher): whether a
+/// kernel was launched at all (empty element ranges launch nothing), how many
+/// independent work teams it started and how many tickets (work units of
+/// per_ticket elements) those teams share through the global work counter
+struct LaunchInfo {
+  int launched = 0;
+  long long teams = 0, tickets = 0;
+  int per_ticket = 0;
+};
+
 struct StageParams {
   long long Kw, Kt;               // all device elements (addressing)
   long long Kw_active, Kt_active; // end of the computed range: owned elements come first, ghosts after
@@ -141,6 +151,7 @@ struct StageParams {
   unsigned long long ticket_base;
   unsigned long long* ticket_host_next; // host side: next base (advanced by the launcher)
   int ticket_batch;                     // consecutive elements per ticket (set by the launcher)
+  LaunchInfo* info;                     // host side, may be null: filled by the launcher
 };
 
 struct EnergyParams {
@@ -195,7 +206,8 @@ cudaError_t launch_pack_states(int N, long long Kw, const long long* dev_elems, 
                                double* buf, cudaStream_t s);
 cudaError_t launch_unpack_states(int N, long long Kw, const long long* dev_elems, long long n, const double* buf,
                                  double* u, cudaStream_t s);
-cudaError_t launch_check_finite(int N, long long Kw, long long Kt, const double* u,
+/// non-finite scan of the owned elements (wedges [0, Kw_act), tets [Kw, Kw + Kt_act))
+cudaError_t launch_check_finite(int N, long long Kw, long long Kw_act, long long Kt_act, const double* u,
                                 const int* dev_to_ref, unsigned long long* first_bad,
                                 cudaStream_t s);
 

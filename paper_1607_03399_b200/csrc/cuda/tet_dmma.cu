@@ -435,6 +435,7 @@ cudaError_t launch_tet_dmma_N(const StageParams& p, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM_BYTES);
     grid_cap[dev] = sms * (per_sm > 0 ? per_sm : 1);
   }
+  if (p.info) *p.info = LaunchInfo{};
   if (p.Kt_active - p.Kt_begin <= 0) return cudaSuccess;
   const long long nbatch = (p.Kt_active - p.Kt_begin + kTB - 1) / kTB;
   const long long need = (nbatch + C::TPB - 1) / C::TPB;
@@ -443,6 +444,7 @@ cudaError_t launch_tet_dmma_N(const StageParams& p, cudaStream_t s) {
   q.ticket_base = *p.ticket_host_next;
   *p.ticket_host_next += (unsigned long long)nbatch + (unsigned long long)grid * C::TPB;
   kern<<<grid, C::THREADS, C::SMEM_BYTES, s>>>(q);
+  if (p.info) *p.info = LaunchInfo{1, (long long)grid * C::TPB, nbatch, kTB};
   return cudaGetLastError();
 }
 

@@ -183,9 +183,11 @@ cudaError_t launch_tet_N(const StageParams& p, cudaStream_t s) {
     if (err != cudaSuccess) return err;
     configured[dev] = true;
   }
+  if (p.info) *p.info = LaunchInfo{};
   if (p.Kt_active - p.Kt_begin <= 0) return cudaSuccess;
   const long long blocks = (p.Kt_active - p.Kt_begin + C::E - 1) / C::E;
   tet_stage_kernel<N><<<(unsigned)blocks, C::THREADS, C::SMEM_BYTES, s>>>(p);
+  if (p.info) *p.info = LaunchInfo{1, blocks, blocks, C::E}; // static blocks, one unit each
   return cudaGetLastError();
 }
 

@@ -655,6 +655,7 @@ cudaError_t launch_dmma_NC(const StageParams& p, cudaStream_t s) {
     grid_cap[dev] = sms * (per_sm > 0 ? per_sm : 1);
   }
   const long long nact = p.Kw_active - p.Kw_begin; // elements of this launch
+  if (p.info) *p.info = LaunchInfo{};
   if (nact <= 0) return cudaSuccess;
   const long long need = (nact + C::TPB - 1) / C::TPB;
   const int grid = (int)(need < grid_cap[dev] ? need : grid_cap[dev]);
@@ -664,6 +665,7 @@ cudaError_t launch_dmma_NC(const StageParams& p, cudaStream_t s) {
   const unsigned long long B = (unsigned long long)q.ticket_batch;
   *p.ticket_host_next += B * (((unsigned long long)nact + B - 1) / B + (unsigned long long)grid * C::TPB);
   kern<<<grid, C::THREADS, C::SMEM_BYTES, s>>>(q);
+  if (p.info) *p.info = LaunchInfo{1, (long long)grid * C::TPB, (nact + (long long)B - 1) / (long long)B, (int)B};
   return cudaGetLastError();
 }
 

@@ -686,6 +686,7 @@ cudaError_t launch_simt_N(const StageParams& p, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::SMEM_BYTES);
     grid_cap[dev] = sms * (per_sm > 0 ? per_sm : 1);
   }
+  if (p.info) *p.info = LaunchInfo{};
   if (p.Kw_active - p.Kw_begin <= 0) return cudaSuccess;
   const long long nchunk = (p.Kw_active - p.Kw_begin + C::E - 1) / C::E;
   const int grid = (int)(nchunk < grid_cap[dev] ? nchunk : grid_cap[dev]);
@@ -694,6 +695,7 @@ cudaError_t launch_simt_N(const StageParams& p, cudaStream_t s) {
   // every CTA grabs until it gets two tickets past the end (one in flight)
   *p.ticket_host_next += (unsigned long long)nchunk + 2ull * (unsigned long long)grid;
   kern<<<grid, C::THREADS, C::SMEM_BYTES, s>>>(q);
+  if (p.info) *p.info = LaunchInfo{1, (long long)grid, nchunk, C::E};
   return cudaGetLastError();
 }
 

@@ -18,7 +18,9 @@ Two partitioners are provided:
   centroids (the device order of one GPU), any wedge/tet mesh;
 * `layered_slab` -- the weak-scaling benchmark mesh (config 5): rank r owns a
   slab of sublayers of a layered wedge mesh; ghosts are the one sublayer below
-  and above, and only triangular faces are cut.
+  and above, and only triangular faces are cut;
+* `layered_strong` -- the strong-scaling one: one fixed layered mesh whose
+  sublayers are split into nranks contiguous z ranges.
 """
 from __future__ import annotations
 
@@ -163,19 +165,21 @@ def layered_global(surface_n: int, slab_interfaces, slab_sublayers, slab_media, 
                                      for (zb, zt, med, _) in layers])
 
 
-def layered_slab(surface_n: int, slab_interfaces, slab_sublayers, slab_media, nranks: int, rank: int,
-                 slab_height: float = 2.0) -> LocalPartition:
-    """Weak-scaling layered mesh (config 5): rank r owns the r-th copy of the slab
-    (stacked in z), plus one ghost sublayer below and above."""
+def _sublayer_partition(surface_n, layers, nranks, rank) -> LocalPartition:
+    """Partition of a stack of single sublayers (z_bottom, z_top, media, owner),
+    owners contiguous and ascending in z: rank r keeps its owned sublayers plus
+    one ghost sublayer below and above; only triangular faces are cut."""
     xy, tris = S.structured_surface(surface_n)
     nv, ntri = xy.shape[0], tris.shape[0]
-    layers = _slab_layers(slab_interfaces, slab_sublayers, slab_media, nranks, slab_height)
-    per = sum(slab_sublayers)
-    first = rank * per - (1 if rank > 0 else 0)
-    last = (rank + 1) * per + (1 if rank < nranks - 1 else 0)  # exclusive
+    owner_of = np.array([lay[3] for lay in layers])
+    mine = np.nonzero(owner_of == rank)[0]
+    if len(mine) == 0:
+        raise ValueError(f"rank {rank} owns no sublayer ({len(layers)} sublayers over {nranks} ranks)")
+    first = int(mine[0]) - (1 if rank > 0 else 0)
+    last = int(mine[-1]) + 1 + (1 if rank < nranks - 1 else 0)  # exclusive
     specs = [S.LayerSpec(np.full(nv, zb), np.full(nv, zt), 1, med) for (zb, zt, med, _) in layers[first:last]]
     lmesh = S.stack_layers(xy, tris, specs)
-    owners = np.repeat([layers[q][3] for q in range(first, last)], ntri)
+    owners = np.repeat(owner_of[first:last], ntri)
     owned = (owners == rank).astype(np.uint8)
     glob = np.arange(first * ntri, last * ntri, dtype=np.int64)
     part = LocalPartition(rank, nranks, lmesh, owned, glob)
@@ -189,6 +193,31 @@ def layered_slab(surface_n: int, slab_interfaces, slab_sublayers, slab_media, nr
         part.send[rank + 1] = top_owned * ntri + tri_ids
         part.recv[rank + 1] = (nlocal - 1) * ntri + tri_ids
     return part
+
+
+def layered_slab(surface_n: int, slab_interfaces, slab_sublayers, slab_media, nranks: int, rank: int,
+                 slab_height: float = 2.0) -> LocalPartition:
+    """Weak-scaling layered mesh (config 5): rank r owns the r-th copy of the slab
+    (stacked in z), plus one ghost sublayer below and above."""
+    layers = _slab_layers(slab_interfaces, slab_sublayers, slab_media, nranks, slab_height)
+    return _sublayer_partition(surface_n, layers, nranks, rank)
+
+
+def layered_strong_layers(slab_interfaces, slab_sublayers, slab_media, nranks: int):
+    """Sublayers of ONE slab (the single-GPU mesh) with contiguous owners: the
+    total work is fixed and the sublayers are split as evenly as possible."""
+    layers = _slab_layers(slab_interfaces, slab_sublayers, slab_media, 1, 0.0)
+    n = len(layers)
+    return [(zb, zt, med, min(q * nranks // n, nranks - 1)) for q, (zb, zt, med, _) in enumerate(layers)]
+
+
+def layered_strong(surface_n: int, slab_interfaces, slab_sublayers, slab_media, nranks: int,
+                   rank: int) -> LocalPartition:
+    """Strong-scaling layered mesh (config 5 strong): the single-domain mesh of
+    `layered_mesh(surface_n, slab_interfaces, slab_sublayers, slab_media)` with
+    its sublayers split into nranks contiguous z ranges."""
+    layers = layered_strong_layers(slab_interfaces, slab_sublayers, slab_media, nranks)
+    return _sublayer_partition(surface_n, layers, nranks, rank)
 
 
 def face_offsets(disc) -> np.ndarray:

@@ -353,6 +353,13 @@ class DeviceContext:
         check(lib().pdg_stage_bytes(self._h, C.byref(wb), C.byref(tb)))
         return wb.value, tb.value
 
+    def launch_info(self):
+        """last wedge / tet stage launch: {launched, teams, tickets, per_ticket} each"""
+        out = np.zeros(8, dtype=np.int64)
+        check(lib().pdg_launch_info(self._h, out.ctypes.data_as(capi.I64P)))
+        keys = ("launched", "teams", "tickets", "per_ticket")
+        return {"wedge": dict(zip(keys, out[:4].tolist())), "tet": dict(zip(keys, out[4:].tolist()))}
+
     def device_order(self):
         out = np.zeros(self.disc.num_elements(), dtype=np.int64)
         check(lib().pdg_device_order(self._h, out.ctypes.data_as(capi.I64P)))
@@ -446,9 +453,11 @@ def run_simulation(disc: Discretization, state: SolutionState, opts: RunOptions,
     log = np.zeros(2 * max_log)
     t = C.c_double(state.time)
     state.u = np.ascontiguousarray(state.u, dtype=np.float64)
-    check(lib().pdg_run_simulation(disc.device().handle, _dp(state.u), C.byref(t), C.byref(o), C.byref(r),
-                                   _dp(log), max_log))
-    state.time = t.value
+    try:
+        check(lib().pdg_run_simulation(disc.device().handle, _dp(state.u), C.byref(t), C.byref(o), C.byref(r),
+                                       _dp(log), max_log))
+    finally:
+        state.time = t.value  # on a watchdog failure: the failure time, like the reference
     n = min(r.num_logged, max_log)
     return RunResult(r.steps, r.dt, r.final_time, r.initial_energy, r.final_energy, r.max_energy_increase,
                      log[: 2 * n].reshape(n, 2))

@@ -187,6 +187,8 @@ def test_watchdog_flags_nan():
     s.u[3] = np.nan
     with pytest.raises(pdg.NumericalError):
         pdg.run_simulation(d, s, pdg.RunOptions(final_time=1.0, watchdog_every=1))
+    # the state is handed back at the failure time (first watchdog, after one step)
+    assert 0.0 < s.time < 1.0 and not np.all(np.isfinite(s.u))
     ctx = d.device()
     ctx.set_state(s.u)
     assert ctx.check_finite() == 0

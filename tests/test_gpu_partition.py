@@ -168,3 +168,31 @@ def test_trace_exchange_with_interior_boundary_split(case, degree):
             seen += 1
         r.close()
     assert seen == d.num_elements()
+
+
+def test_partitioned_context_refuses_whole_domain_calls():
+    """A partitioned context's ghosts are only current right after the caller's
+    exchange: whole-step / rhs / phase / assembly entries refuse it; the watchdog
+    scans owned elements only (a NaN planted in a ghost is not reported)."""
+    part = P.layered_slab(4, [-1.0, 0.0, 1.0], [2, 3], [(1.0, 1.0), (1.0, 4.0)], 2, 0)
+    r = Rank(part, 2)
+    try:
+        n = r.disc.total_dofs
+        u = np.zeros(n)
+        ghost = int(np.nonzero(part.owned == 0)[0][0])
+        off = r.disc.elem_offset()
+        u[off[ghost]] = np.nan
+        check(lib().pdg_set_state(r.ctx, u.ctypes.data_as(capi.DP), 0))
+        bad = C.c_int64()
+        check(lib().pdg_check_finite(r.ctx, C.byref(bad)))
+        assert bad.value == -1
+        assert lib().pdg_step_lserk(r.ctx, 1e-3, 1, None) == capi.PDG_ERR_CONFIG
+        out = np.zeros(n)
+        assert lib().pdg_rhs(r.ctx, u.ctypes.data_as(capi.DP), out.ctypes.data_as(capi.DP), 0) == capi.PDG_ERR_CONFIG
+        assert lib().pdg_wedge_volume(r.ctx) == capi.PDG_ERR_CONFIG
+        # the per-stage entry the distributed driver uses still works
+        u[off[ghost]] = 0.0
+        check(lib().pdg_set_state(r.ctx, u.ctypes.data_as(capi.DP), 0))
+        check(lib().pdg_step_stage(r.ctx, 1e-3, 0))
+    finally:
+        r.close()

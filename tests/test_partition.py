@@ -119,6 +119,8 @@ def make_partition(case, world, rank):
         return P.partition_mesh(pdg.structured_hybrid_box(3, 3, 2, 2, (1.0, 1.0), (1.0, 4.0)), world, rank)
     if case == "unstructured":
         return P.partition_mesh(pdg.make_family_mesh("unstructured", 0.5), world, rank)
+    if case == "strong":
+        return P.layered_strong(4, [-1.0, 0.0, 1.0], [2, 3], [(1.0, 1.0), (1.0, 4.0)], world, rank)
     return P.layered_slab(4, [-1.0, 0.0, 1.0], [2, 3], [(1.0, 1.0), (1.0, 4.0)], world, rank)
 
 
@@ -127,11 +129,14 @@ def global_mesh(case, world):
         return pdg.structured_hybrid_box(3, 3, 2, 2, (1.0, 1.0), (1.0, 4.0))
     if case == "unstructured":
         return pdg.make_family_mesh("unstructured", 0.5)
+    if case == "strong":
+        return P.layered_global(4, [-1.0, 0.0, 1.0], [2, 3], [(1.0, 1.0), (1.0, 4.0)], 1)
     return P.layered_global(4, [-1.0, 0.0, 1.0], [2, 3], [(1.0, 1.0), (1.0, 4.0)], world)
 
 
 @pytest.mark.parametrize("case,mode", [("hybrid", "elements"), ("unstructured", "elements"), ("layered", "elements"),
-                                       ("hybrid", "traces"), ("unstructured", "traces"), ("layered", "traces")])
+                                       ("hybrid", "traces"), ("unstructured", "traces"), ("layered", "traces"),
+                                       ("strong", "traces")])
 def test_two_rank_lserk_matches_single_domain(case, mode, tmp_path):
     """Whole-element ghost refresh and face-trace-only refresh (the GPU path's) both
     reproduce the single-domain run bit for bit: the RHS reads nothing else of a ghost."""
