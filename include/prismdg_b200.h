@@ -101,6 +101,63 @@ int pdg_disc_build(const pdg_mesh* mesh, int degree, int flux_mode, double tau_p
 int pdg_disc_build_ex(const pdg_mesh* mesh, int degree, int flux_mode, double tau_p, double tau_u,
                       int mass_mode, int threads, int flags, pdg_disc** out);
 int pdg_disc_get_info(const pdg_disc* d, pdg_disc_info* info);
+
+/* A Discretization assembled from arrays the CALLER built -- the reference's
+ * own Discretization (solver.hpp:29-59) flattened member by member, so the
+ * device path runs on the reference's Eigen-built operators instead of this
+ * library's host setup (export_to_pdg).  Layouts:
+ * wedges first, then tets (mesh.hpp:25,36); nt = (N+1)(N+2)/2, nq = N+1;
+ * faces in (element, face) order, 5 per wedge then 4 per tet;
+ * max_nfp = max(nq*nq, nt).  Matrices are column-major (Eigen's default).
+ * The shared reference data (References, reference.hpp:13-112: nodes,
+ * derivative matrices, face-node lists, lift profiles) is rebuilt from the
+ * degree -- the same construction, pinned against the reference's own unit
+ * tests -- and the caller's face-node lists are checked against it. */
+typedef struct pdg_disc_arrays {
+  int degree;
+  int qmode;            /* QuadratureMode (operators.hpp:17): 0 exact, 1 lumped; 2 = weight-adjusted */
+  int flux_mode;        /* FluxConfig (solver.hpp:17-20), recorded; the per-face tau below are used */
+  double tau_p, tau_u;
+  /* HybridMesh (mesh.hpp:22-41) */
+  int64_t num_vertices, num_wedges, num_tets;
+  const double* vertices; /* [nv][3] */
+  const int* wedges;      /* [nw][6], 0-based */
+  const int* tets;        /* [ntet][4], 0-based */
+  const double* media;    /* [ne][2] = {rho, kappa} */
+  /* geom (ElementGeometry, geometry.hpp:20-38): per wedge {j0, j_r, j_s, volume,
+   * surface_area, faces[2..4].jf_edge[0], .jf_edge[N]} (11); per tet {J (= j0),
+   * volume, surface_area} (3) */
+  const double* wedge_geom;
+  const double* tet_geom;
+  /* wedge_ops (WedgeOperators, operators.hpp:22-33) */
+  const double* tri_lift;      /* [nw][nt*nt], tri_lift(i,k) at [k*nt + i]; may be NULL when qmode == 2 */
+  const double* quad_lift;     /* [nw][3][nq*nt], quad_lift[e](i,a) at [(e*nq + a)*nt + i]; NULL when qmode == 2 */
+  const double* txJ;           /* [nw][nq] */
+  const double* tyJ;           /* [nw][nq] */
+  const double* wedge_scalars; /* [nw][7] = {tzJ, rx, ry, sx, sy, jf_bottom, jf_top} */
+  /* tet_ops (TetOperators, operators.hpp:37-42): [ntet][13] = {rx, ry, rz, sx, sy, sz, tx, ty, tz, lift_scale[4]} */
+  const double* tet_scalars;
+  /* face_data (Discretization::FaceData, solver.hpp:52-58) */
+  const int* face_nbr;          /* [nfaces]: neighbour element, -1 = boundary (reflective) */
+  const double* face_tau;       /* [nfaces][2] = {tau_p, tau_u} */
+  const double* face_normal;    /* [nfaces][3] */
+  const int* face_my_nodes;     /* [nfaces][max_nfp] or NULL (= the reference face-node lists) */
+  const int* face_nbr_nodes;    /* [nfaces][max_nfp]: neighbour local volume node of my face node i */
+} pdg_disc_arrays;
+
+/* Validates (sizes, face maps onto a neighbour face, positive J) and copies;
+ * the arrays may be freed afterwards.  PDG_ERR_CONFIG / PDG_ERR_MESH on bad input. */
+int pdg_disc_from_arrays(const pdg_disc_arrays* a, pdg_disc** out);
+/* The inverse: fill caller buffers with the per-element arrays of
+ * the pdg_disc_arrays struct, same layouts; any pointer may be NULL; mesh arrays via
+ * pdg_disc_mesh_export, lifts via pdg_disc_wedge_ops. */
+int pdg_disc_export_arrays(const pdg_disc* d, double* wedge_geom, double* tet_geom, double* txJ, double* tyJ,
+                           double* wedge_scalars, double* tet_scalars, int* face_nbr, double* face_tau,
+                           double* face_normal, int* face_nbr_nodes);
+/* the mesh a discretization was built on (sizes from pdg_disc_get_info /
+ * pdg_disc_mesh_counts); any pointer may be NULL */
+int pdg_disc_mesh_export(const pdg_disc* d, int64_t counts[3], double* vertices, int* wedges, int* tets,
+                         double* media);
 /* Discretization::elem_offset (solver.hpp:44), num_elements+1 entries */
 int pdg_disc_elem_offset(const pdg_disc* d, int64_t* out);
 /* per element face in (element, face) order: neighbour element (-1 boundary),

@@ -14,7 +14,7 @@ from .solver import (Discretization, DeviceContext, HybridMesh, LayerSpec, RunOp
                      estimate_dt, fit_rate, l2_error, layered_mesh, load_mesh, make_family_mesh,
                      make_initial_state, perturb_vertically, run_simulation, spectra_mesh, stack_layers,
                      structured_hybrid_box, structured_surface, structured_wedge_box, unstructured_wedge_box,
-                     write_vtk_snapshot)
+                     write_vtk_snapshot, export_arrays, discretization_from_arrays)
 
 capi.lib()  # load now: no silent fallback
 

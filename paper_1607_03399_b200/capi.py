@@ -68,6 +68,22 @@ class DiscInfo(C.Structure):
     ]
 
 
+class DiscArrays(C.Structure):
+    """pdg_disc_arrays: the reference's Discretization flattened (solver.hpp:29-59)."""
+    _fields_ = [
+        ("degree", C.c_int), ("qmode", C.c_int), ("flux_mode", C.c_int), ("tau_p", C.c_double),
+        ("tau_u", C.c_double), ("num_vertices", C.c_int64), ("num_wedges", C.c_int64), ("num_tets", C.c_int64),
+        ("vertices", C.POINTER(C.c_double)), ("wedges", C.POINTER(C.c_int)), ("tets", C.POINTER(C.c_int)),
+        ("media", C.POINTER(C.c_double)), ("wedge_geom", C.POINTER(C.c_double)),
+        ("tet_geom", C.POINTER(C.c_double)), ("tri_lift", C.POINTER(C.c_double)),
+        ("quad_lift", C.POINTER(C.c_double)), ("txJ", C.POINTER(C.c_double)), ("tyJ", C.POINTER(C.c_double)),
+        ("wedge_scalars", C.POINTER(C.c_double)), ("tet_scalars", C.POINTER(C.c_double)),
+        ("face_nbr", C.POINTER(C.c_int)), ("face_tau", C.POINTER(C.c_double)),
+        ("face_normal", C.POINTER(C.c_double)), ("face_my_nodes", C.POINTER(C.c_int)),
+        ("face_nbr_nodes", C.POINTER(C.c_int)),
+    ]
+
+
 SNAPSHOT_CB = C.CFUNCTYPE(None, C.POINTER(C.c_double), C.c_double, C.c_int, C.c_void_p)
 
 
@@ -127,6 +143,9 @@ SIGNATURES = {
     "pdg_disc_l2_error": (C.c_int, [P, DP, C.c_double, DP]),
     "pdg_disc_wedge_ops": (C.c_int, [P, C.c_int64, DP, DP, DP]),
     "pdg_disc_free": (None, [P]),
+    "pdg_disc_from_arrays": (C.c_int, [C.POINTER(DiscArrays), PP]),
+    "pdg_disc_export_arrays": (C.c_int, [P, DP, DP, DP, DP, DP, DP, IP, DP, DP, IP]),
+    "pdg_disc_mesh_export": (C.c_int, [P, I64P, DP, IP, IP, DP]),
     "pdg_create": (C.c_int, [P, C.c_int, C.c_int, PP]),
     "pdg_destroy": (None, [P]),
     "pdg_set_state": (C.c_int, [P, P, C.c_int]),

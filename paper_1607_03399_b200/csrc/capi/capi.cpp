@@ -378,6 +378,99 @@ int pdg_write_vtk(const pdg_disc* dh, const double* u, const char* path) {
   });
 }
 
+int pdg_disc_from_arrays(const pdg_disc_arrays* a, pdg_disc** out) {
+  return guarded([&] {
+    need(a, "arrays");
+    need(out, "output");
+    *out = reinterpret_cast<pdg_disc*>(new Discretization(discretization_from_arrays(*a)));
+  });
+}
+
+int pdg_disc_export_arrays(const pdg_disc* dh, double* wedge_geom, double* tet_geom, double* txJ, double* tyJ,
+                           double* wedge_scalars, double* tet_scalars, int* face_nbr, double* face_tau,
+                           double* face_normal, int* face_nbr_nodes) {
+  return guarded([&] {
+    need(dh, "discretization");
+    const Discretization& d = *D(dh);
+    const int nw = d.mesh.num_wedges(), ntet = d.mesh.num_tets(), nq = d.nq;
+    for (int w = 0; w < nw; ++w) {
+      const WedgeGeo& g = d.wgeo[w];
+      if (wedge_geom) {
+        const double v[11] = {g.j0, g.jr, g.js, g.volume, g.surface_area, g.jf_quad[0][0], g.jf_quad[0][1],
+                              g.jf_quad[1][0], g.jf_quad[1][1], g.jf_quad[2][0], g.jf_quad[2][1]};
+        std::copy(v, v + 11, wedge_geom + 11 * (std::size_t)w);
+      }
+      if (wedge_scalars) {
+        const double v[7] = {g.tzJ, g.rx, g.ry, g.sx, g.sy, g.jf_bottom, g.jf_top};
+        std::copy(v, v + 7, wedge_scalars + 7 * (std::size_t)w);
+      }
+      for (int j = 0; j < nq; ++j) {
+        if (txJ) txJ[(std::size_t)w * nq + j] = d.txJ[(std::size_t)w * nq + j];
+        if (tyJ) tyJ[(std::size_t)w * nq + j] = d.tyJ[(std::size_t)w * nq + j];
+      }
+    }
+    for (int t = 0; t < ntet; ++t) {
+      const TetGeo& g = d.tgeo[t];
+      if (tet_geom) {
+        tet_geom[3 * (std::size_t)t] = g.J;
+        tet_geom[3 * (std::size_t)t + 1] = g.volume;
+        tet_geom[3 * (std::size_t)t + 2] = g.surface_area;
+      }
+      if (tet_scalars) {
+        const double v[13] = {g.rx, g.ry, g.rz, g.sx, g.sy, g.sz, g.tx, g.ty, g.tz,
+                              g.lift_scale[0], g.lift_scale[1], g.lift_scale[2], g.lift_scale[3]};
+        std::copy(v, v + 13, tet_scalars + 13 * (std::size_t)t);
+      }
+    }
+    const int max_nfp = std::max(d.nq * d.nq, d.nt);
+    for (int e = 0; e < d.num_elements(); ++e)
+      for (int f = 0; f < d.mesh.num_faces(e); ++f) {
+        const std::size_t q = (std::size_t)d.conn.face_offset[e] + f;
+        const FaceConn& fc = d.conn.faces[q];
+        if (face_nbr) face_nbr[q] = fc.nbr;
+        if (face_tau) {
+          face_tau[2 * q] = d.fphys[q].tau_p;
+          face_tau[2 * q + 1] = d.fphys[q].tau_u;
+        }
+        if (face_normal)
+          for (int c = 0; c < 3; ++c) face_normal[3 * q + c] = d.fphys[q].normal[c];
+        if (face_nbr_nodes) {
+          int* row = face_nbr_nodes + q * max_nfp;
+          std::fill(row, row + max_nfp, -1);
+          if (fc.nbr >= 0)
+            for (int i = 0; i < (int)d.my_nodes(e, f).size(); ++i) row[i] = d.nbr_node(e, f, i);
+        }
+      }
+  });
+}
+
+int pdg_disc_mesh_export(const pdg_disc* dh, int64_t counts[3], double* vertices, int* wedges, int* tets,
+                         double* media) {
+  return guarded([&] {
+    need(dh, "discretization");
+    const HybridMesh& m = D(dh)->mesh;
+    if (counts) {
+      counts[0] = (int64_t)m.vertices.size();
+      counts[1] = m.num_wedges();
+      counts[2] = m.num_tets();
+    }
+    if (vertices)
+      for (std::size_t v = 0; v < m.vertices.size(); ++v)
+        for (int c = 0; c < 3; ++c) vertices[3 * v + c] = m.vertices[v][c];
+    if (wedges)
+      for (int w = 0; w < m.num_wedges(); ++w)
+        for (int c = 0; c < 6; ++c) wedges[6 * (std::size_t)w + c] = m.wedges[w][c];
+    if (tets)
+      for (int t = 0; t < m.num_tets(); ++t)
+        for (int c = 0; c < 4; ++c) tets[4 * (std::size_t)t + c] = m.tets[t][c];
+    if (media)
+      for (int e = 0; e < m.num_elements(); ++e) {
+        media[2 * (std::size_t)e] = m.media[e].rho;
+        media[2 * (std::size_t)e + 1] = m.media[e].kappa;
+      }
+  });
+}
+
 void pdg_disc_free(pdg_disc* d) { delete reinterpret_cast<Discretization*>(d); }
 
 // ------------------------------------------------------------------ device

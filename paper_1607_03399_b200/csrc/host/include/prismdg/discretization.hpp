@@ -19,6 +19,8 @@
 #include <memory>
 #include <vector>
 
+struct pdg_disc_arrays; // include/prismdg_b200.h
+
 namespace prismdg {
 
 enum class FluxMode { upwind = 0, central = 1, custom = 2 };
@@ -103,5 +105,9 @@ struct Discretization {
 Discretization build_discretization(HybridMesh mesh, int degree, FluxConfig flux = {},
                                     QuadratureMode qmode = QuadratureMode::exact, int threads = 1,
                                     MassMode mass_mode = MassMode::exact, bool with_quad_lift = true);
+
+/// A Discretization from a caller's flattened arrays (pdg_disc_arrays,
+/// include/prismdg_b200.h; csrc/host/disc_ingest.cpp)
+Discretization discretization_from_arrays(const ::pdg_disc_arrays& a);
 
 } // namespace prismdg

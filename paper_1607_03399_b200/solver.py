@@ -248,6 +248,67 @@ class Discretization:
         return self._ctx
 
 
+DISC_ARRAY_FIELDS = ("vertices", "wedges", "tets", "media", "wedge_geom", "tet_geom", "tri_lift", "quad_lift", "txJ",
+                     "tyJ", "wedge_scalars", "tet_scalars", "face_nbr", "face_tau", "face_normal", "face_my_nodes",
+                     "face_nbr_nodes")
+
+
+def export_arrays(disc: "Discretization") -> dict:
+    """The flattened per-element arrays of pdg_disc_arrays (the reference's
+    Discretization members, solver.hpp:29-59) of an existing discretization."""
+    info = disc.info
+    N, nq, nt = info.degree, info.nq, info.nt
+    nw, ntet, nf = int(info.num_wedges), int(info.num_tets), int(info.num_faces)
+    max_nfp = max(nq * nq, nt)
+    cnt = np.zeros(3, dtype=np.int64)
+    check(lib().pdg_disc_mesh_export(disc.handle, cnt.ctypes.data_as(capi.I64P), None, None, None, None))
+    a = {"degree": N, "qmode": {0: 0, 1: 1, 2: 2}[info.mass_mode], "flux_mode": info.flux_mode,
+         "vertices": np.zeros((int(cnt[0]), 3)), "wedges": np.zeros((nw, 6), np.int32),
+         "tets": np.zeros((ntet, 4), np.int32), "media": np.zeros((nw + ntet, 2)),
+         "wedge_geom": np.zeros((nw, 11)), "tet_geom": np.zeros((ntet, 3)), "txJ": np.zeros((nw, nq)),
+         "tyJ": np.zeros((nw, nq)), "wedge_scalars": np.zeros((nw, 7)), "tet_scalars": np.zeros((ntet, 13)),
+         "face_nbr": np.zeros(nf, np.int32), "face_tau": np.zeros((nf, 2)), "face_normal": np.zeros((nf, 3)),
+         "face_nbr_nodes": np.zeros((nf, max_nfp), np.int32)}
+    check(lib().pdg_disc_mesh_export(disc.handle, None, _dp(a["vertices"]), _ip(a["wedges"]), _ip(a["tets"]),
+                                     _dp(a["media"])))
+    check(lib().pdg_disc_export_arrays(disc.handle, _dp(a["wedge_geom"]), _dp(a["tet_geom"]), _dp(a["txJ"]),
+                                       _dp(a["tyJ"]), _dp(a["wedge_scalars"]), _dp(a["tet_scalars"]),
+                                       _ip(a["face_nbr"]), _dp(a["face_tau"]), _dp(a["face_normal"]),
+                                       _ip(a["face_nbr_nodes"])))
+    if nw and info.mass_mode != 2:
+        a["tri_lift"] = np.zeros((nw, nt * nt))
+        a["quad_lift"] = np.zeros((nw, 3 * nq * nt))
+        for w in range(nw):
+            check(lib().pdg_disc_wedge_ops(disc.handle, w, _dp(a["tri_lift"][w]), _dp(a["quad_lift"][w]), None))
+    return a
+
+
+def discretization_from_arrays(arrays: dict, mesh=None) -> "Discretization":
+    """pdg_disc_from_arrays: a Discretization from a caller's flattened arrays
+    (e.g. the reference's own Eigen-built operators)."""
+    s = capi.DiscArrays()
+    s.degree = int(arrays["degree"])
+    s.qmode = int(arrays.get("qmode", 0))
+    s.flux_mode = int(arrays.get("flux_mode", 0))
+    s.tau_p = float(arrays.get("tau_p", 0.0))
+    s.tau_u = float(arrays.get("tau_u", 0.0))
+    keep = {}
+    for name in DISC_ARRAY_FIELDS:
+        v = arrays.get(name)
+        if v is None:
+            continue
+        is_int = name in ("wedges", "tets", "face_nbr", "face_my_nodes", "face_nbr_nodes")
+        arr = np.ascontiguousarray(v, dtype=np.int32 if is_int else np.float64)
+        keep[name] = arr
+        setattr(s, name, arr.ctypes.data_as(capi.IP if is_int else capi.DP))
+    s.num_vertices = len(keep["vertices"])
+    s.num_wedges = len(keep["wedges"]) if "wedges" in keep else 0
+    s.num_tets = len(keep["tets"]) if "tets" in keep else 0
+    out = C.c_void_p()
+    check(lib().pdg_disc_from_arrays(C.byref(s), C.byref(out)))
+    return Discretization(out.value, mesh)
+
+
 def build_discretization(mesh: HybridMesh, degree: int, flux="upwind", tau_p=0.0, tau_u=0.0,
                          mass="exact", threads=0, host_lifts=True) -> Discretization:
     """build_discretization (solver.hpp:61-63).  mass: "exact" | "lumped" | "wadg".
