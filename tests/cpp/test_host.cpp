@@ -664,6 +664,55 @@ TEST(spectra_mesh_size) {
   CHECK(d.total_dofs == 1152);
 }
 
+TEST(dt_estimate_scaling_and_cfl_check) {
+  // test_solver.cpp:86-98: dt doubles with the mesh, halves with c = 2; cfl < 0 throws
+  const Discretization d1 = small_box(2, 2);
+  HybridMesh scaled = structured_wedge_box(2);
+  for (auto& v : scaled.vertices)
+    for (auto& c : v) c *= 2.0;
+  const Discretization d2 = build_discretization(std::move(scaled), 2, {}, QuadratureMode::exact, 1);
+  CHECK_CLOSE(estimate_dt(d2, 0.5), 2.0 * estimate_dt(d1, 0.5), 1e-12);
+  const Discretization d3 = build_discretization(structured_wedge_box(2, {1.0, 4.0}), 2, {}, QuadratureMode::exact, 1);
+  CHECK_CLOSE(estimate_dt(d3, 0.5), 0.5 * estimate_dt(d1, 0.5), 1e-12);
+  CHECK_THROWS(estimate_dt(d1, -1.0), ConfigError);
+}
+
+TEST(time_stepper_orders_scalar) {
+  // test_solver.cpp:113-144: y' = lambda y, lambda = -0.4 + 1.3i, dt = 0.1, 0.05,
+  // 0.025 to t = 1; order from dt halving: LSERK45 4 +- 8%, AB3 3 +- 8%
+  const double lr = -0.4, li = 1.3;
+  auto order_of = [&](IntegratorKind kind) {
+    std::vector<double> errs;
+    for (const double dt : {0.1, 0.05, 0.025}) {
+      std::vector<double> y = {1.0, 0.0};
+      double t = 0.0;
+      TimeStepper st(kind, 2);
+      const RhsFn rhs = [&](const std::vector<double>& u, std::vector<double>& out, double) {
+        out.resize(2);
+        out[0] = lr * u[0] - li * u[1];
+        out[1] = li * u[0] + lr * u[1];
+      };
+      const int steps = (int)std::lround(1.0 / dt);
+      for (int i = 0; i < steps; ++i) st.step(y, t, dt, rhs, nullptr);
+      const double er = std::exp(lr) * std::cos(li), ei = std::exp(lr) * std::sin(li);
+      errs.push_back(std::hypot(y[0] - er, y[1] - ei));
+    }
+    return std::log2(errs[0] / errs[2]) / 2.0;
+  };
+  const double o4 = order_of(IntegratorKind::lserk4), o3 = order_of(IntegratorKind::ab3);
+  std::printf("    lserk4 order %.3f, ab3 order %.3f\n", o4, o3);
+  CHECK(std::abs(o4 - 4.0) <= 0.32);
+  CHECK(std::abs(o3 - 3.0) <= 0.24);
+}
+
+TEST(oracle_zero_rhs_fixes_state) {
+  // test_solver.cpp:113-122: a zero state stays exactly zero through a step
+  const Discretization d = small_box(1, 1);
+  std::vector<double> u(d.total_dofs, 0.0);
+  oracle::lserk_steps(d, u.data(), u.size(), 0.01, 1, 1, false);
+  for (double v : u) CHECK(v == 0.0);
+}
+
 int main(int argc, char** argv) {
   const char* filter = argc > 1 ? argv[1] : nullptr;
   int ran = 0;

@@ -1,0 +1,139 @@
+"""The reference's acceptance criteria 1, 2 and 4 (proj/tests/acceptance.cpp:40-186)
+and its solver unit tests test_solver.cpp:100-200, run through the GPU driver
+(pdg_run_simulation) at the reference's own sizes -- the three mesh families
+down to h = 0.125 -- plus the device integrators' temporal order measured
+against the exact propagator of the assembled DG operator."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1607_03399_b200 as pdg
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+H = [2.0, 1.0, 0.5, 0.25, 0.125]
+
+
+def run_error(mesh, degree, final_time=1.0):
+    """convergence_study's inner loop (analysis.cpp:140-165): standing wave to
+    t = 1 with the estimated dt, energy at the endpoints, L2 pressure error;
+    NaN when the watchdog fires."""
+    d = pdg.build_discretization(mesh, degree)
+    s = pdg.make_initial_state(d)
+    try:
+        pdg.run_simulation(d, s, pdg.RunOptions(final_time=final_time, energy_interval=final_time))
+    except pdg.NumericalError:
+        return float("nan")
+    return pdg.l2_error(d, s.u, s.time)
+
+
+# acceptance.cpp:44-48
+RATES = {"structured": (2.01, 3.15, 3.97), "unstructured": (1.72, 2.9, 4.42), "arnold": (1.9, 3.13, 3.99)}
+
+
+@pytest.mark.parametrize("family", sorted(RATES))
+@pytest.mark.parametrize("degree", [1, 2, 3])
+def test_criterion1_convergence_rates(family, degree):
+    """Criterion 1: the fitted rate over h = 2 .. 0.125 (last three points,
+    fit_rate analysis.cpp:126-139) within +-0.3 of the reference table."""
+    errs = [run_error(pdg.make_family_mesh(family, h), degree) for h in H]
+    assert all(np.isfinite(errs)), errs
+    rate = pdg.fit_rate(H, errs)
+    assert abs(rate - RATES[family][degree - 1]) <= 0.3, (family, degree, rate, errs)
+    if family == "structured":
+        gold = json.load(open(os.path.join(HERE, "golden", "paper_convergence.json")))["structured_errors"]
+        for k, h in enumerate(H):
+            ref = gold[str(degree)][k] if k < len(gold[str(degree)]) else None
+            if ref is not None and h <= 0.5:
+                assert abs(errs[k] - ref) <= 1e-2 * ref, (degree, h, errs[k], ref)
+
+
+def test_criterion2_absolute_errors():
+    """Criterion 2 (acceptance.cpp:76-97): structured h = 0.125 (8,192 wedges),
+    N = 2 and 3 errors within a x3 band of 6.91e-5 and 1.7e-6."""
+    e2 = run_error(pdg.make_family_mesh("structured", 0.125), 2)
+    e3 = run_error(pdg.make_family_mesh("structured", 0.125), 3)
+    assert 6.91e-5 / 3 < e2 < 3 * 6.91e-5, e2
+    assert 1.7e-6 / 3 < e3 < 3 * 1.7e-6, e3
+
+
+@pytest.mark.parametrize("name", ["wedge box", "hybrid box", "tet box", "perturbed"])
+@pytest.mark.parametrize("degree", [1, 2, 3, 4])
+def test_criterion4_upwind_energy_non_increasing(name, degree):
+    """Criterion 4, first half (acceptance.cpp:139-160): upwind runs to t = 0.4
+    never gain energy between logged steps, on every suite mesh."""
+    mesh = {"wedge box": lambda: pdg.structured_wedge_box(2),
+            "hybrid box": lambda: pdg.structured_hybrid_box(2, 2, 1, 1),
+            "tet box": lambda: pdg.structured_hybrid_box(2, 2, 0, 2),
+            "perturbed": lambda: pdg.spectra_mesh()}[name]()
+    d = pdg.build_discretization(mesh, degree)
+    s = pdg.make_initial_state(d)
+    res = pdg.run_simulation(d, s, pdg.RunOptions(final_time=0.4))
+    assert res.max_energy_increase <= 1e-10 * res.initial_energy, res
+
+
+@pytest.mark.parametrize("mesh_fn", [lambda: pdg.structured_wedge_box(2), lambda: pdg.structured_hybrid_box(2, 2, 1, 1)])
+def test_criterion4_central_drift_order(mesh_fn):
+    """Criterion 4, second half / test_solver.cpp:164-179: with the central flux
+    the energy drift shrinks at >= 3.7 orders under dt halving (LSERK45)."""
+    d = pdg.build_discretization(mesh_fn(), 2, flux="central")
+    dt0 = pdg.estimate_dt(d, 0.5)
+    drift = []
+    for level in range(3):
+        s = pdg.make_initial_state(d)
+        res = pdg.run_simulation(d, s, pdg.RunOptions(final_time=0.5, fixed_dt=dt0 / (1 << level),
+                                                      energy_interval=0.5))
+        drift.append(abs(res.final_energy - res.initial_energy))
+    slope = np.log2(drift[0] / drift[2]) / 2.0
+    assert slope >= 3.7, (slope, drift)
+
+
+def test_thousand_step_bounded_run():
+    """test_solver.cpp:100-111: 1000 steps at the default cfl, energy every 100
+    steps, watchdog on; the energy ends no higher than it started."""
+    d = pdg.build_discretization(pdg.structured_wedge_box(2), 2)
+    s = pdg.make_initial_state(d)
+    dt = pdg.estimate_dt(d, 0.5)
+    res = pdg.run_simulation(d, s, pdg.RunOptions(final_time=1000 * dt, fixed_dt=dt, energy_interval=100 * dt))
+    assert res.steps == 1000
+    assert res.final_energy <= res.initial_energy * (1.0 + 1e-10)
+
+
+def test_media_jump_layer_interface_is_stable():
+    """test_solver.cpp:181-200: two layers (kappa 1 | 4) over a 2-triangle square,
+    2 sublayers each, gaussian pulse to t = 1: upwind energy never grows."""
+    xy = np.array([[-1, -1], [1, -1], [1, 1], [-1, 1]], dtype=float)
+    tris = np.array([[0, 1, 2], [0, 2, 3]], dtype=np.int32)
+    layers = [pdg.LayerSpec(np.full(4, -1.0), np.full(4, 0.0), 2, (1.0, 1.0)),
+              pdg.LayerSpec(np.full(4, 0.0), np.full(4, 1.0), 2, (1.0, 4.0))]
+    d = pdg.build_discretization(pdg.stack_layers(xy, tris, layers), 2)
+    s = pdg.make_initial_state(d, "gaussian", [0.4, 0.0, 0.0, 0.0])
+    res = pdg.run_simulation(d, s, pdg.RunOptions(final_time=1.0))
+    assert res.max_energy_increase <= 1e-10 * res.initial_energy
+
+
+@pytest.mark.parametrize("integrator,order", [("lserk4", 4.0), ("ab3", 3.0)])
+def test_device_integrator_order(integrator, order):
+    """test_solver.cpp:113-144 on the device integrators: u' = A u with A the
+    assembled DG operator of the 1152-DOF spectra mesh, stepped by the fused
+    LSERK45 stage kernels / the device AB3 update against expm(A T) u0; the
+    error shrinks at the integrator's order (+-8%) under dt halving."""
+    from scipy.linalg import expm
+    d = pdg.build_discretization(pdg.spectra_mesh(), 2)
+    A = pdg.assemble_global(d)
+    u0 = pdg.make_initial_state(d).u
+    T = 0.4
+    exact = expm(A * T) @ u0
+    dt0 = pdg.estimate_dt(d, 0.5) * (0.25 if integrator == "ab3" else 1.0)
+    errs = []
+    for level in range(3):
+        steps = int(np.ceil(T / (dt0 / (1 << level))))
+        ctx = d.device()
+        ctx.set_state(u0)
+        ctx.step(T / steps, steps, integrator=integrator)
+        errs.append(np.linalg.norm(ctx.get_state() - exact))
+    got = np.log2(errs[0] / errs[2]) / 2.0
+    assert abs(got - order) <= 0.08 * order, (got, errs)
