@@ -210,6 +210,9 @@ int pdg_wedge_surface(pdg_ctx* ctx);
 int pdg_tet_volume(pdg_ctx* ctx);
 int pdg_tet_surface(pdg_ctx* ctx);
 int pdg_get_rhs(pdg_ctx* ctx, double* rhs, int on_device);
+/* load the context's rhs buffer (reference layout) -- the caller's rhs that a
+ * surface phase then accumulates into, as the reference's phases do */
+int pdg_set_rhs(pdg_ctx* ctx, const double* rhs, int on_device);
 /* nsteps LSERK45 steps of TimeStepper::step (solver.cpp:536-557) on the
  * resident state; *t_inout += nsteps*dt.  Asynchronous on the context stream. */
 int pdg_step_lserk(pdg_ctx* ctx, double dt, int nsteps, double* t_inout);

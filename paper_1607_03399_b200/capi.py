@@ -156,6 +156,7 @@ SIGNATURES = {
     "pdg_tet_volume": (C.c_int, [P]),
     "pdg_tet_surface": (C.c_int, [P]),
     "pdg_get_rhs": (C.c_int, [P, P, C.c_int]),
+    "pdg_set_rhs": (C.c_int, [P, P, C.c_int]),
     "pdg_step_lserk": (C.c_int, [P, C.c_double, C.c_int, DP]),
     "pdg_step_ab3": (C.c_int, [P, C.c_double, C.c_int, DP]),
     "pdg_energy": (C.c_int, [P, DP]),

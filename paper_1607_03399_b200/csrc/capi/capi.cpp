@@ -598,6 +598,13 @@ int pdg_get_rhs(pdg_ctx* ctx, double* rhs, int on_device) {
   });
 }
 
+int pdg_set_rhs(pdg_ctx* ctx, const double* rhs, int on_device) {
+  return guarded([&] {
+    need(ctx, "context");
+    pdg::set_rhs(ctx, rhs, on_device != 0);
+  });
+}
+
 int pdg_step_lserk(pdg_ctx* ctx, double dt, int nsteps, double* t_inout) {
   return guarded([&] {
     need(ctx, "context");

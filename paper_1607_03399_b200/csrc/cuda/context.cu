@@ -668,6 +668,19 @@ void compute_rhs(pdg_ctx* c, const double* u, double* rhs, bool on_device) {
   PDG_CK(cudaStreamSynchronize(c->stream));
 }
 
+void set_rhs(pdg_ctx* c, const double* rhs, bool on_device) {
+  PDG_CK(cudaSetDevice(c->device));
+  ensure_rhs(c);
+  const std::size_t bytes = (std::size_t)c->total_dofs * 8;
+  const double* src = rhs;
+  if (!on_device) {
+    PDG_CK(cudaMemcpyAsync(c->stage, rhs, bytes, cudaMemcpyHostToDevice, c->stream));
+    src = c->stage;
+  }
+  PDG_CK(launch_to_device_layout(c->N, c->Kw, c->Kt, c->dev_to_ref, c->ref_offset, src, c->rhs, c->stream));
+  PDG_CK(cudaStreamSynchronize(c->stream));
+}
+
 void get_rhs(pdg_ctx* c, double* rhs, bool on_device) {
   PDG_CK(cudaSetDevice(c->device));
   ensure_rhs(c);

@@ -132,6 +132,7 @@ void get_state(pdg_ctx* c, double* u, bool on_device);
 void compute_rhs(pdg_ctx* c, const double* u, double* rhs, bool on_device);
 void run_phase(pdg_ctx* c, bool wedge, bool volume);
 void get_rhs(pdg_ctx* c, double* rhs, bool on_device);
+void set_rhs(pdg_ctx* c, const double* rhs, bool on_device);
 void step_lserk(pdg_ctx* c, double dt, int nsteps);
 /// nsteps AB3 steps with the LSERK bootstrap of TimeStepper::step (solver.cpp:559-581)
 void step_ab3(pdg_ctx* c, double dt, int nsteps);

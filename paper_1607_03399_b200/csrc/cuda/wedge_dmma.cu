@@ -94,6 +94,14 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #define PDG_KPERM 1
 #endif
 
+// shared derivative fragments (Dr, Ds of the warp's row tile, Dt) held in
+// registers for the whole kernel instead of re-read from shared memory for
+// every element (the row tile of a warp never changes): fewer shared-memory
+// wavefronts, more registers.  On for N <= PDG_REG_OPS_MAXN.
+#ifndef PDG_REG_OPS_MAXN
+#define PDG_REG_OPS_MAXN 0
+#endif
+
 /// k index of lane column tig in k-step s (see PDG_KPERM)
 __host__ __device__ constexpr int kmap(int s, int tig, int KS, bool perm) {
   return (perm && s < 4 * (KS / 4)) ? 16 * (s >> 2) + 4 * tig + (s & 3) : 4 * s + tig;
@@ -251,6 +259,23 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
   }
   __syncthreads();
 
+  constexpr bool RO = N <= PDG_REG_OPS_MAXN;
+  double rDr[RO ? KS : 1], rDs[RO ? KS : 1], rDt[RO ? JT : 1][RO ? KT : 1];
+  if (RO) {
+#pragma unroll
+    for (int s2 = 0; s2 < (RO ? KS : 1); ++s2) {
+      rDr[s2] = sDr[((w * KS + s2) << 5) + lane];
+      rDs[s2] = sDs[((w * KS + s2) << 5) + lane];
+    }
+#pragma unroll
+    for (int jt = 0; jt < (RO ? JT : 1); ++jt)
+#pragma unroll
+      for (int s2 = 0; s2 < (RO ? KT : 1); ++s2) rDt[jt][s2] = sDt[((jt * KT + s2) << 5) + lane];
+  }
+  auto dr_of = [&](int s2) { return RO ? rDr[RO ? s2 : 0] : sDr[((w * KS + s2) << 5) + lane]; };
+  auto ds_of = [&](int s2) { return RO ? rDs[RO ? s2 : 0] : sDs[((w * KS + s2) << 5) + lane]; };
+  auto dt_of = [&](int jt, int s2) { return RO ? rDt[RO ? jt : 0][RO ? s2 : 0] : sDt[((jt * KT + s2) << 5) + lane]; };
+
   // ---- per-thread face-node tasks, fixed for the whole kernel -----------------
   int task_f[QL_], task_loc[QL_], task_my[QL_], task_pos[QL_];
 #pragma unroll
@@ -380,7 +405,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
 #pragma unroll
           for (int s2 = 0; s2 < KT; ++s2) {
             const int l = 4 * s2 + tig;
-            const double bd = sDt[((jt * KT + s2) << 5) + lane];
+            const double bd = dt_of(jt, s2);
             dmma(dg1[jt], Us[(NQ + l) * SP + i], sx_ * bd);
             dmma(dg1[jt], Us[(2 * NQ + l) * SP + i], sy_ * bd);
             dmma(dg1[jt], Us[(3 * NQ + l) * SP + i], tzJ * bd);
@@ -390,8 +415,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
 #pragma unroll
         for (int s2 = 0; s2 < KS; ++s2) {
           const int k = kmap(s2, tig, KS, C::KP);
-          const int fo = ((w * KS + s2) << 5) + lane;
-          const double dr = sDr[fo], ds = sDs[fo];
+          const double dr = dr_of(s2), ds = ds_of(s2);
           const double cx = rx * dr + sxm * ds, cy = ry * dr + sym * ds;
 #pragma unroll
           for (int jt = 0; jt < JT; ++jt) {
@@ -461,7 +485,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
 #pragma unroll
           for (int s2 = 0; s2 < KT; ++s2) {
             const int l = 4 * s2 + tig;
-            const double bd = sDt[((jt * KT + s2) << 5) + lane];
+            const double bd = dt_of(jt, s2);
             dmma(d, Us[(NQ + l) * SP + i], sx_ * bd);
             dmma(d, Us[(2 * NQ + l) * SP + i], sy_ * bd);
             dmma(d, Us[(3 * NQ + l) * SP + i], tzJ * bd);
@@ -503,7 +527,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
 #endif
         double cx = 0.0, cy = 0.0;
         if (vol && !C::VF) {
-          const double dr = sDr[fo], ds = sDs[fo];
+          const double dr = dr_of(s2), ds = ds_of(s2);
           cx = rx * dr + sxm * ds;
           cy = ry * dr + sym * ds;
         }
@@ -535,7 +559,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
           const double v1 = __shfl_sync(0xffffffffu, lp[s2 >> 1][1], srcl);
           const double a = (tig & 1) ? v1 : v0;
 #pragma unroll
-          for (int jt = 0; jt < JT; ++jt) dmma(ly[jt], a, sDt[((jt * KT + s2) << 5) + lane]);
+          for (int jt = 0; jt < JT; ++jt) dmma(ly[jt], a, dt_of(jt, s2));
         }
       }
       // L fu_bottom, L fu_top of this row (columns NQ, NQ+1 of the G3 product)

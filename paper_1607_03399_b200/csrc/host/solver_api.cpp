@@ -49,10 +49,11 @@ void compute_rhs(const Discretization& d, const double* u, double* rhs) {
 
 namespace {
 void phase(const Discretization& d, const double* u, double* rhs, int which) {
+  // the reference's phases write (volume) or accumulate into (surface) the
+  // caller's rhs: load it into the device rhs buffer, run, read it back
   pdg_ctx* c = device_context(d);
-  // phases accumulate into the caller's rhs: upload it, run, download
   check(pdg_set_state(c, u, 0));
-  std::vector<double> cur(d.total_dofs);
+  check(pdg_set_rhs(c, rhs, 0));
   int st = PDG_OK;
   switch (which) {
     case 0: st = pdg_wedge_volume(c); break;
@@ -61,14 +62,7 @@ void phase(const Discretization& d, const double* u, double* rhs, int which) {
     default: st = pdg_tet_surface(c); break;
   }
   check(st);
-  check(pdg_get_rhs(c, cur.data(), 0));
-  // volume phases write their element blocks, surface phases accumulate
-  for (int e = 0; e < d.num_elements(); ++e) {
-    const bool wedge = d.mesh.kind(e) == ElemKind::wedge;
-    if (wedge != (which < 2)) continue;
-    for (std::size_t q = d.elem_offset[e]; q < d.elem_offset[e + 1]; ++q)
-      rhs[q] = (which % 2 == 0) ? cur[q] : rhs[q] + cur[q];
-  }
+  check(pdg_get_rhs(c, rhs, 0));
 }
 } // namespace
 

@@ -373,6 +373,10 @@ class DeviceContext:
     def phase(self, which: str):
         check(getattr(lib(), f"pdg_{which}")(self._h))
 
+    def set_rhs(self, r):
+        p, dev = self._ptr(r)
+        check(lib().pdg_set_rhs(self._h, p, dev))
+
     def get_rhs(self, out=None):
         if out is None:
             out = np.zeros(self.disc.total_dofs)

@@ -34,21 +34,48 @@ def run_error(mesh, degree, final_time=1.0):
 RATES = {"structured": (2.01, 3.15, 3.97), "unstructured": (1.72, 2.9, 4.42), "arnold": (1.9, 3.13, 3.99)}
 
 
+def oracle_error(mesh, degree, final_time=1.0):
+    """the same run on the CPU oracle (reference algorithm, serial update)"""
+    import oracle_binding as ob
+    d = pdg.build_discretization(mesh, degree)
+    s = pdg.make_initial_state(d)
+    u, t, res = ob.run(d, s.u, 0.0, final_time, cfl=0.5, energy_interval=final_time, threads=os.cpu_count() or 4)
+    return pdg.l2_error(d, u, t)
+
+
 @pytest.mark.parametrize("family", sorted(RATES))
 @pytest.mark.parametrize("degree", [1, 2, 3])
 def test_criterion1_convergence_rates(family, degree):
     """Criterion 1: the fitted rate over h = 2 .. 0.125 (last three points,
-    fit_rate analysis.cpp:126-139) within +-0.3 of the reference table."""
+    fit_rate analysis.cpp:126-139) within +-0.3 of the reference table; the
+    GPU errors equal the CPU oracle's (the reference algorithm on the same,
+    bit-identical meshes) at h = 2 .. 0.25."""
     errs = [run_error(pdg.make_family_mesh(family, h), degree) for h in H]
     assert all(np.isfinite(errs)), errs
+    for k, h in enumerate(H[:4]):
+        want = oracle_error(pdg.make_family_mesh(family, h), degree)
+        assert abs(errs[k] - want) <= 1e-8 * want, (family, degree, h, errs[k], want)
     rate = pdg.fit_rate(H, errs)
-    assert abs(rate - RATES[family][degree - 1]) <= 0.3, (family, degree, rate, errs)
+    gold = json.load(open(os.path.join(HERE, "golden", "paper_convergence.json")))
+    if (family, degree) == ("unstructured", 3):
+        # The table's 4.42 is not what the paper's own error column gives (its
+        # last three points fit 3.38), and the reference's pseudo-random meshes
+        # (mt19937_64, reproduced bit for bit here) give 3.88 -- on the GPU and
+        # on the CPU oracle alike, so the reference itself lands there too.
+        want = oracle_error(pdg.make_family_mesh(family, 0.125), degree)
+        assert abs(errs[4] - want) <= 1e-8 * want
+        assert abs(rate - RATES[family][degree - 1]) <= 0.6, (rate, errs)
+        ref = gold["unstructured_errors"]["3"]
+        assert all(r / 3 < e < 3 * r for e, r in zip(errs, ref)), (errs, ref)
+    else:
+        assert abs(rate - RATES[family][degree - 1]) <= 0.3, (family, degree, rate, errs)
     if family == "structured":
-        gold = json.load(open(os.path.join(HERE, "golden", "paper_convergence.json")))["structured_errors"]
         for k, h in enumerate(H):
-            ref = gold[str(degree)][k] if k < len(gold[str(degree)]) else None
-            if ref is not None and h <= 0.5:
+            ref = gold["structured_errors"][str(degree)][k]
+            if 0.25 <= h <= 0.5:  # published with >= 3 significant digits: 1 %
                 assert abs(errs[k] - ref) <= 1e-2 * ref, (degree, h, errs[k], ref)
+            elif h == 0.125:  # 6.91e-5 / 1.7e-6: the reference's own x3 band (acceptance.cpp:91-93)
+                assert ref / 3 < errs[k] < 3 * ref, (degree, h, errs[k], ref)
 
 
 def test_criterion2_absolute_errors():
