@@ -191,6 +191,9 @@ void pdg_disc_free(pdg_disc* d);
 /* ---------------------------------------------------------------- device path */
 #define PDG_CTX_NATIVE_ORDER 1 /* keep reference element order on device (no Morton) */
 #define PDG_CTX_TIMING 2       /* bracket every stage kernel with CUDA events      */
+/* multi-rate AB3: group the elements into up to L+1 rate levels by their
+ * local stable step (level g steps with 2^g dt), for pdg_step_mrab */
+#define PDG_CTX_MRAB_LEVELS(L) (((L) & 15) << 8)
 
 /* Upload a discretization to `device`. Replaces the first use of the host
  * Discretization by compute_rhs / TimeStepper (solver.cpp:362-377, 536-557). */
@@ -221,6 +224,18 @@ int pdg_step_lserk(pdg_ctx* ctx, double dt, int nsteps, double* t_inout);
  * (bootstrap), then u += dt/12 (23 f_n - 16 f_{n-1} + 5 f_{n-2}).  The f
  * history lives on the device and is reset by pdg_set_state. */
 int pdg_step_ab3(pdg_ctx* ctx, double dt, int nsteps, double* t_inout);
+/* nmacro steps of the multi-rate Adams-Bashforth 3 integrator (the paper's
+ * time integrator, after Goedel et al. 2010; not in the
+ * reference code) on a context created with
+ * PDG_CTX_MRAB_LEVELS(L).  Level g advances with 2^g dt, a macro step is
+ * 2^(levels-1) fine steps of dt (*t_inout += that).  The first two macro
+ * steps after pdg_set_state are LSERK45 steps at dt that fill every level's
+ * history (the reference's AB3 bootstrap, solver.cpp:563-570).  With one
+ * level this is exactly pdg_step_ab3.  Stability: dt <= AB3's step
+ * (estimate_dt * 0.25, solver.hpp:114). */
+int pdg_step_mrab(pdg_ctx* ctx, double dt, int nmacro, double* t_inout);
+/* rate level of every reference element (-1 when multi-rate is off); *nlevels */
+int pdg_mrab_levels(pdg_ctx* ctx, int* level, int* nlevels);
 /* compute_energy (solver.hpp:78): deterministic device reduction */
 int pdg_energy(pdg_ctx* ctx, double* energy);
 /* watchdog scan (solver.cpp:647-655): first element (reference id) with a
@@ -299,7 +314,9 @@ typedef struct {
   double energy_interval; /* 0: log every step */
   int watchdog_every;
   double blowup_factor;
-  int integrator;         /* 0 lserk4, 1 ab3 (dt = estimate * 0.25, solver.hpp:114) */
+  int integrator;         /* 0 lserk4, 1 ab3 (dt = estimate * 0.25, solver.hpp:114),
+                             2 multi-rate AB3 (context with PDG_CTX_MRAB_LEVELS; the step
+                             counted is the macro step, fine dt = estimate * 0.25) */
   /* snapshots (RunOptions::snapshot_interval / snapshot_cb, solver.cpp:625-644):
    * at the start and whenever the time passes the next multiple of the
    * interval the state (reference layout) is streamed device -> pinned host

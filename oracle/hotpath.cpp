@@ -475,6 +475,69 @@ void ab3_steps(const Discretization& d, double* u, std::size_t n, double dt, int
   }
 }
 
+void mrab_steps(const Discretization& d, double* u, std::size_t n, const int* level, int nlev, double dt, int nmacro,
+                int threads) {
+  // Multi-rate AB3 restated element by element (the device's pdg_step_mrab;
+  // PAPER.md:614).  Level g steps with h_g = 2^g dt, M = 2^(nlev-1) fine
+  // substeps per macro step; the first two macro steps are LSERK45 at dt with
+  // f_g recorded at t - h_g and t - 2 h_g (ab3_steps' bootstrap per level).
+  const int M = 1 << (nlev - 1), ne = d.num_elements();
+  std::vector<std::vector<double>> f(3, std::vector<double>(n, 0.0));
+  std::vector<double> u0(n), r(n);
+  std::vector<std::array<int, 3>> slot(nlev, std::array<int, 3>{0, 1, 2});
+  auto for_level = [&](int g, auto&& fn) {
+    for (int e = 0; e < ne; ++e)
+      if (level[e] == g)
+        for (std::size_t i = d.elem_offset[e]; i < d.elem_offset[e + 1]; ++i) fn(i);
+  };
+  for (int m = 0; m < nmacro; ++m) {
+    if (m < 2) {
+      for (int k = 0; k < M; ++k) {
+        const int nb = m * M + k;
+        bool need = false;
+        for (int g = 0; g < nlev; ++g) need = need || nb == 2 * M - (1 << g) || nb == 2 * M - (2 << g);
+        if (need) {
+          compute_rhs(d, u, r.data(), threads);
+          for (int g = 0; g < nlev; ++g) {
+            if (nb == 2 * M - (1 << g)) for_level(g, [&](std::size_t i) { f[slot[g][1]][i] = r[i]; });
+            if (nb == 2 * M - (2 << g)) for_level(g, [&](std::size_t i) { f[slot[g][2]][i] = r[i]; });
+          }
+        }
+        lserk_steps(d, u, n, dt, 1, threads, false);
+      }
+      if (m == 1) std::copy(u, u + n, u0.begin());
+      continue;
+    }
+    for (int k = 0; k < M; ++k) {
+      bool any = false;
+      for (int g = 0; g < nlev; ++g) any = any || k % (1 << g) == 0;
+      if (any) compute_rhs(d, u, r.data(), threads);  // per element: identical to a per-level rhs
+      for (int g = 0; g < nlev; ++g)
+        if (k % (1 << g) == 0) for_level(g, [&](std::size_t i) { f[slot[g][0]][i] = r[i]; });
+      for (int g = 0; g < nlev; ++g) {
+        const int kk = k % (1 << g);
+        const double h = std::ldexp(dt, g), th = (double)(kk + 1) / (1 << g);
+        const double* f0 = f[slot[g][0]].data();
+        const double* f1 = f[slot[g][1]].data();
+        const double* f2 = f[slot[g][2]].data();
+        if (kk + 1 == (1 << g)) {
+          for_level(g, [&](std::size_t i) {
+            const double v = u0[i] + (h / 12.0) * (23.0 * f0[i] - 16.0 * f1[i] + 5.0 * f2[i]);
+            u[i] = v;
+            u0[i] = v;
+          });
+          slot[g] = {slot[g][2], slot[g][0], slot[g][1]};
+        } else {
+          // integral over [0, th] of the backward-difference quadratic through f0, f1, f2
+          const double c0 = th + 0.75 * th * th + th * th * th / 6.0, c1 = -th * th - th * th * th / 3.0,
+                       c2 = 0.25 * th * th + th * th * th / 6.0;
+          for_level(g, [&](std::size_t i) { u[i] = u0[i] + h * (c0 * f0[i] + c1 * f1[i] + c2 * f2[i]); });
+        }
+      }
+    }
+  }
+}
+
 RunOut run_simulation(const Discretization& d, std::vector<double>& u, double& time, double final_time, double cfl,
                       double fixed_dt, double energy_interval, int threads) {
   // solver.cpp:591-666 (LSERK, watchdog every 50 steps, blow-up factor 10)

@@ -59,6 +59,12 @@ void lserk_steps(const Discretization& d, double* u, std::size_t n, double dt, i
 /// (solver.cpp:559-581): two LSERK45 bootstrap steps recording f, then AB3
 void ab3_steps(const Discretization& d, double* u, std::size_t n, double dt, int nsteps, int threads);
 
+/// nmacro multi-rate AB3 macro steps (pdg_step_mrab's algorithm): level[e] in
+/// [0, nlev) is element e's rate level (step 2^level dt); the first two macro
+/// steps are the LSERK45 bootstrap at dt
+void mrab_steps(const Discretization& d, double* u, std::size_t n, const int* level, int nlev, double dt, int nmacro,
+                int threads);
+
 struct RunOut {
   int steps = 0;
   double dt = 0, final_time = 0, initial_energy = 0, final_energy = 0, max_energy_increase = 0;

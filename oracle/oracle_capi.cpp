@@ -62,6 +62,10 @@ int orc_ab3(const void* disc, double* u, double dt, int nsteps, int threads) {
   return guard([&] { oracle::ab3_steps(*D(disc), u, D(disc)->total_dofs, dt, nsteps, threads); });
 }
 
+int orc_mrab(const void* disc, double* u, const int* level, int nlev, double dt, int nmacro, int threads) {
+  return guard([&] { oracle::mrab_steps(*D(disc), u, D(disc)->total_dofs, level, nlev, dt, nmacro, threads); });
+}
+
 int orc_energy(const void* disc, const double* u, int threads, double* out) {
   return guard([&] { *out = oracle::compute_energy(*D(disc), u, threads); });
 }

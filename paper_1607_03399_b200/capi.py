@@ -29,6 +29,11 @@ CTX_NATIVE_ORDER = 1
 CTX_TIMING = 2
 
 
+def CTX_MRAB_LEVELS(levels: int) -> int:
+    """PDG_CTX_MRAB_LEVELS(L): up to L+1 multi-rate levels"""
+    return (levels & 15) << 8
+
+
 class PdgError(RuntimeError):
     """Base class; subclasses mirror the reference exception taxonomy (types.hpp:14-34)."""
 
@@ -159,6 +164,8 @@ SIGNATURES = {
     "pdg_set_rhs": (C.c_int, [P, P, C.c_int]),
     "pdg_step_lserk": (C.c_int, [P, C.c_double, C.c_int, DP]),
     "pdg_step_ab3": (C.c_int, [P, C.c_double, C.c_int, DP]),
+    "pdg_step_mrab": (C.c_int, [P, C.c_double, C.c_int, DP]),
+    "pdg_mrab_levels": (C.c_int, [P, IP, IP]),
     "pdg_energy": (C.c_int, [P, DP]),
     "pdg_check_finite": (C.c_int, [P, I64P]),
     "pdg_synchronize": (C.c_int, [P]),

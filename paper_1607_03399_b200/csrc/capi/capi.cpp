@@ -615,6 +615,27 @@ int pdg_step_lserk(pdg_ctx* ctx, double dt, int nsteps, double* t_inout) {
   });
 }
 
+int pdg_step_mrab(pdg_ctx* ctx, double dt, int nmacro, double* t_inout) {
+  return guarded([&] {
+    need(ctx, "context");
+    if (!(dt > 0.0)) throw ConfigError("dt must be positive");
+    if (nmacro < 0) throw ConfigError("nmacro must be >= 0");
+    pdg::step_mrab(ctx, dt, nmacro);
+    if (t_inout) *t_inout += nmacro * std::ldexp(dt, std::max(ctx->mr_nlev - 1, 0));
+  });
+}
+
+int pdg_mrab_levels(pdg_ctx* ctx, int* level, int* nlevels) {
+  return guarded([&] {
+    need(ctx, "context");
+    if (nlevels) *nlevels = ctx->mr_nlev;
+    if (level) {
+      const long long ne = ctx->Kw + ctx->Kt;
+      for (long long e = 0; e < ne; ++e) level[e] = ctx->mr_nlev ? ctx->mr_level_ref[e] : -1;
+    }
+  });
+}
+
 int pdg_step_ab3(pdg_ctx* ctx, double dt, int nsteps, double* t_inout) {
   return guarded([&] {
     need(ctx, "context");
@@ -707,13 +728,17 @@ int pdg_run_simulation(pdg_ctx* ctx, double* u_inout, double* time_inout, const 
   return guarded([&] {
     need(ctx, "context");
     need(opts, "options");
-    if (opts->integrator != 0 && opts->integrator != 1) throw ConfigError("unknown integrator");
-    const bool ab3 = opts->integrator == 1;
+    if (opts->integrator < 0 || opts->integrator > 2) throw ConfigError("unknown integrator");
+    const bool ab3 = opts->integrator >= 1, mrab = opts->integrator == 2;
+    if (mrab && ctx->mr_nlev == 0)
+      throw ConfigError("the multi-rate integrator needs a context created with PDG_CTX_MRAB_LEVELS(L)");
+    const int substeps = mrab ? 1 << (ctx->mr_nlev - 1) : 1; // fine steps per (macro) step
     if (!(opts->final_time > *time_inout)) throw ConfigError("final time must exceed the state time");
     if (opts->watchdog_every < 1) throw ConfigError("watchdog_every must be >= 1");
     const double span = opts->final_time - *time_inout;
     // TimeStepper::dt_scale (solver.hpp:114): AB3 runs at a quarter of the LSERK step
-    const double dt0 = opts->fixed_dt > 0.0 ? opts->fixed_dt : estimate_dt(*ctx->disc, opts->cfl) * (ab3 ? 0.25 : 1.0);
+    const double dt0 = opts->fixed_dt > 0.0 ? opts->fixed_dt
+                                            : estimate_dt(*ctx->disc, opts->cfl) * (ab3 ? 0.25 : 1.0) * substeps;
     const int steps = std::max(1, (int)std::ceil(span / dt0 - 1e-12));
     const double dt = span / steps;
     pdg::set_state(ctx, u_inout, false);
@@ -760,7 +785,9 @@ int pdg_run_simulation(pdg_ctx* ctx, double* u_inout, double* time_inout, const 
       }
     } on_throw{ctx, u_inout, time_inout, &t};
     for (int n = 0; n < steps; ++n) {
-      if (ab3)
+      if (mrab)
+        pdg::step_mrab(ctx, dt / substeps, 1);
+      else if (ab3)
         pdg::step_ab3(ctx, dt, 1);
       else
         pdg::step_lserk(ctx, dt, 1);

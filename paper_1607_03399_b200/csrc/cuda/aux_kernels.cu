@@ -141,6 +141,30 @@ __global__ void ab3_update_kernel(long long n, double* __restrict__ u, const dou
     u[idx] += c * (23.0 * f0[idx] - 16.0 * f1[idx] + 5.0 * f2[idx]);
 }
 
+// multi-rate AB3 (MRAB) update of one rate level, over its wedge DOF range
+// [w0, w1) and tet DOF range [t0, t1) (levels are contiguous in device order):
+//   commit (end of the level's step): u = u0 = u0 + h/12 (23 f0 - 16 f1 + 5 f2),
+//     the single-rate AB3 formula (solver.cpp:575-577) from the step start;
+//   predict (mid-step, read by finer neighbours): u = u0 + h (c0 f0 + c1 f1 + c2 f2),
+//     the AB3 interpolant of the level's rhs history integrated over [0, theta h]
+__global__ void mrab_update_kernel(long long w0, long long w1, long long t0, long long t1, double* __restrict__ u,
+                                   double* __restrict__ u0, const double* __restrict__ f0,
+                                   const double* __restrict__ f1, const double* __restrict__ f2, double h,
+                                   double c0, double c1, double c2, int commit) {
+  const long long nw = w1 - w0, n = nw + (t1 - t0);
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long idx = q < nw ? w0 + q : t0 + (q - nw);
+    if (commit) {
+      const double v = u0[idx] + (h / 12.0) * (23.0 * f0[idx] - 16.0 * f1[idx] + 5.0 * f2[idx]);
+      u[idx] = v;
+      u0[idx] = v;
+    } else {
+      u[idx] = u0[idx] + h * (c0 * f0[idx] + c1 * f1[idx] + c2 * f2[idx]);
+    }
+  }
+}
+
 __global__ void reduce_sum_kernel(const double* __restrict__ in, int n, double* __restrict__ out) {
   // single block, fixed order: strided partial sums then a tree
   __shared__ double red[1024];
@@ -288,6 +312,20 @@ cudaError_t launch_ab3_update(long long n, double* u, const double* f0, const do
                               double dt, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   ab3_update_kernel<<<148 * 8, 256, 0, s>>>(n, u, f0, f1, f2, dt / 12.0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mrab_update(long long w0, long long w1, long long t0, long long t1, double* u, double* u0,
+                               const double* f0, const double* f1, const double* f2, double h, double theta,
+                               int commit, cudaStream_t s) {
+  const long long n = (w1 - w0) + (t1 - t0);
+  if (n <= 0) return cudaSuccess;
+  // int_0^theta of the backward-difference quadratic through f0 (s=0), f1 (s=-1), f2 (s=-2)
+  const double th = theta, th2 = th * th, th3 = th2 * th;
+  const double c0 = th + 0.75 * th2 + th3 / 6.0, c1 = -th2 - th3 / 3.0, c2 = 0.25 * th2 + th3 / 6.0;
+  const long long want = (n + 255) / 256;
+  const int grid = (int)(want < 148 * 8 ? want : 148 * 8);
+  mrab_update_kernel<<<grid, 256, 0, s>>>(w0, w1, t0, t1, u, u0, f0, f1, f2, h, c0, c1, c2, commit);
   return cudaGetLastError();
 }
 

@@ -312,6 +312,41 @@ pdg_ctx* create_context(const prismdg::Discretization& d, int device, int flags,
     c->Kt_act = c->Kt;
     c->Kw_int = c->Kw;
     c->Kt_int = c->Kt;
+    const int mr_extra = (flags >> 8) & 15;
+    if (mr_extra > 0) {
+      // multi-rate levels from the local stable step h_e / c_e (h = volume /
+      // surface area, estimate_dt's per-element term, solver.cpp:437-447):
+      // level g holds the elements whose step is >= 2^g times the smallest
+      if (owned) throw prismdg::ConfigError("multi-rate stepping on a partitioned context is not supported");
+      const int ne = d.num_elements(), nw = d.mesh.num_wedges();
+      std::vector<double> rate(ne);
+      double rmin = std::numeric_limits<double>::max();
+      for (int e = 0; e < ne; ++e) {
+        const double h = e < nw ? d.wgeo[e].volume / d.wgeo[e].surface_area
+                                : d.tgeo[e - nw].volume / d.tgeo[e - nw].surface_area;
+        rate[e] = h / d.mesh.media[e].wavespeed();
+        rmin = std::min(rmin, rate[e]);
+      }
+      c->mr_level_ref.assign(ne, 0);
+      int top = 0;
+      for (int e = 0; e < ne; ++e) {
+        int g = 0;
+        while (g < mr_extra && rate[e] >= std::ldexp(rmin, g + 1) * (1.0 - 1e-12)) ++g;
+        c->mr_level_ref[e] = g;
+        top = std::max(top, g);
+      }
+      c->mr_nlev = top + 1;
+      auto by_level = [&](std::vector<long long>& ord, std::vector<long long>& bounds, long long base) {
+        std::stable_sort(ord.begin(), ord.end(),
+                         [&](long long a, long long b) { return c->mr_level_ref[a] < c->mr_level_ref[b]; });
+        bounds.assign(c->mr_nlev + 1, 0);
+        for (long long r : ord) ++bounds[c->mr_level_ref[r] + 1];
+        for (int g = 0; g < c->mr_nlev; ++g) bounds[g + 1] += bounds[g];
+        (void)base;
+      };
+      by_level(word, c->mr_w, 0);
+      by_level(tord, c->mr_t, nw);
+    }
     if (owned) {
       // owned interior (no ghost neighbour) first, then owned boundary, then
       // ghosts; stable, so each group keeps the locality order.  The interior
@@ -587,7 +622,7 @@ void destroy_context(pdg_ctx* c) {
                   c->tgeo, c->tconn, c->DrT, c->DsT, c->Dt, c->prof, c->wface_dev, c->tDrT,
                   c->tDsT, c->tDtT, c->tLiftT, c->tface, c->nbr_nodes, c->Mtri, c->Xr, c->Xs,
                   c->M1D, c->w1d, c->Mtet, c->partials, c->scalar, c->badflag, c->ticket, c->dev_to_ref,
-                  c->fh[0], c->fh[1], c->fh[2],
+                  c->fh[0], c->fh[1], c->fh[2], c->mr_u0, c->mr_tmp,
                   c->ref_offset};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -605,6 +640,7 @@ void set_state(pdg_ctx* c, const double* u, bool on_device) {
   }
   PDG_CK(launch_to_device_layout(c->N, c->Kw, c->Kt, c->dev_to_ref, c->ref_offset, src, c->u[c->cur], c->stream));
   c->ab3_filled = 0; // a new state starts a new AB3 history
+  c->mr_boot = 0;     // ... and a new multi-rate bootstrap
 }
 
 void get_state(pdg_ctx* c, double* u, bool on_device) {
@@ -746,6 +782,103 @@ void step_ab3(pdg_ctx* c, double dt, int nsteps) {
     c->fh[2] = c->fh[1];
     c->fh[1] = c->fh[0];
     c->fh[0] = f2;
+  }
+}
+
+void step_mrab(pdg_ctx* c, double dt, int nmacro) {
+  // Multi-rate Adams-Bashforth 3 (the paper's integrator, after
+  // Goedel et al. 2010): level g advances with h_g = 2^g dt; a macro step is
+  // M = 2^L fine substeps.  At substep k every level starting a step (k mod
+  // 2^g == 0) evaluates its rhs (reading the current / predicted states of its
+  // neighbours); then each level either commits its AB3 step or writes the
+  // AB3 predictor at theta = (k mod 2^g + 1) / 2^g for the finer levels that
+  // read it next.  Bootstrap: the first two macro steps are LSERK45 at dt
+  // (the reference's AB3 bootstrap, solver.cpp:563-570, per level), recording
+  // f_g at t - h_g and t - 2 h_g.
+  PDG_CK(cudaSetDevice(c->device));
+  require_unpartitioned(c, "multi-rate AB3");
+  if (c->mr_nlev == 0)
+    throw prismdg::ConfigError("multi-rate stepping needs a context created with PDG_CTX_MRAB_LEVELS(L)");
+  const std::size_t nd = (std::size_t)c->dev_dofs;
+  for (auto& h : c->fh)
+    if (!h) {
+      h = dalloc<double>(nd);
+      PDG_CK(cudaMemsetAsync(h, 0, nd * 8, c->stream));
+    }
+  if (!c->mr_u0) {
+    c->mr_u0 = dalloc<double>(nd);
+    c->mr_tmp = dalloc<double>(nd);
+    PDG_CK(cudaMemsetAsync(c->mr_tmp, 0, nd * 8, c->stream));
+  }
+  const int nlev = c->mr_nlev, M = 1 << (nlev - 1);
+  const long long wblk = 4LL * npd_of(c->N), tblk = 4LL * c->npt;
+  auto wr = [&](int g, long long& a, long long& b) {
+    a = c->mr_w[g] * wblk;
+    b = c->mr_w[g + 1] * wblk;
+  };
+  auto tr = [&](int g, long long& a, long long& b) {
+    a = c->tet_base + c->mr_t[g] * tblk;
+    b = c->tet_base + c->mr_t[g + 1] * tblk;
+  };
+  auto copy_level = [&](int g, const double* src, double* dst) {
+    long long a, b;
+    wr(g, a, b);
+    if (b > a) PDG_CK(cudaMemcpyAsync(dst + a, src + a, (b - a) * 8, cudaMemcpyDeviceToDevice, c->stream));
+    tr(g, a, b);
+    if (b > a) PDG_CK(cudaMemcpyAsync(dst + a, src + a, (b - a) * 8, cudaMemcpyDeviceToDevice, c->stream));
+  };
+  for (int m = 0; m < nmacro; ++m) {
+    if (c->mr_boot < 2) {
+      if (c->mr_boot == 0)
+        for (int g = 0; g < nlev; ++g) c->mr_slot[g][0] = 0, c->mr_slot[g][1] = 1, c->mr_slot[g][2] = 2;
+      for (int k = 0; k < M; ++k) {
+        const int nb = c->mr_boot * M + k;
+        bool need = false;
+        for (int g = 0; g < nlev; ++g) need = need || nb == 2 * M - (1 << g) || nb == 2 * M - (2 << g);
+        if (need) {
+          rhs_into(c, c->mr_tmp);
+          for (int g = 0; g < nlev; ++g) {
+            if (nb == 2 * M - (1 << g)) copy_level(g, c->mr_tmp, c->fh[c->mr_slot[g][1]]);
+            if (nb == 2 * M - (2 << g)) copy_level(g, c->mr_tmp, c->fh[c->mr_slot[g][2]]);
+          }
+        }
+        step_lserk(c, dt, 1);
+      }
+      if (++c->mr_boot == 2)
+        PDG_CK(cudaMemcpyAsync(c->mr_u0, c->u[c->cur], nd * 8, cudaMemcpyDeviceToDevice, c->stream));
+      continue;
+    }
+    for (int k = 0; k < M; ++k) {
+      for (int g = 0; g < nlev; ++g) {
+        if (k % (1 << g) != 0) continue;
+        StageParams p = base_params(c);
+        p.u_in = c->u[c->cur];
+        p.rhs_out = c->fh[c->mr_slot[g][0]];
+        p.mode = M_VOLUME | M_SURFACE | M_MEDIA;
+        p.Kw_begin = c->mr_w[g];
+        p.Kw_active = c->mr_w[g + 1];
+        p.Kt_begin = c->mr_t[g];
+        p.Kt_active = c->mr_t[g + 1];
+        launch_checked(c, p, true);
+        launch_checked(c, p, false);
+      }
+      for (int g = 0; g < nlev; ++g) {
+        const int kk = k % (1 << g);
+        const bool commit = kk + 1 == (1 << g);
+        long long w0, w1, t0, t1;
+        wr(g, w0, w1);
+        tr(g, t0, t1);
+        int* sl = c->mr_slot[g];
+        PDG_CK(launch_mrab_update(w0, w1, t0, t1, c->u[c->cur], c->mr_u0, c->fh[sl[0]], c->fh[sl[1]], c->fh[sl[2]],
+                                  std::ldexp(dt, g), (double)(kk + 1) / (1 << g), commit ? 1 : 0, c->stream));
+        if (commit) {
+          const int f2 = sl[2];
+          sl[2] = sl[1];
+          sl[1] = sl[0];
+          sl[0] = f2;
+        }
+      }
+    }
   }
 }
 

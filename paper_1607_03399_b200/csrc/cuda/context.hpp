@@ -73,6 +73,17 @@ struct pdg_ctx {
 
   pdg::LaunchInfo last_launch[2]; // most recent wedge / tet stage launch
 
+  // multi-rate AB3 (PDG_CTX_MRAB_LEVELS): rate level g steps with 2^g dt;
+  // levels are contiguous in device order: wedges [mr_w[g], mr_w[g+1]),
+  // tets Kw + [mr_t[g], mr_t[g+1])
+  int mr_nlev = 0;
+  std::vector<long long> mr_w, mr_t;
+  std::vector<int> mr_level_ref;   // level of every reference element
+  double* mr_u0 = nullptr;         // state at each level's current step start
+  double* mr_tmp = nullptr;        // bootstrap rhs
+  int mr_slot[16][3] = {};         // per level: fh index of f_n, f_{n-1}, f_{n-2}
+  int mr_boot = 0;                 // bootstrap macro steps done (2 = running)
+
   double wedge_bytes_first = 0.0, wedge_bytes_later = 0.0;
   double tet_bytes_first = 0.0, tet_bytes_later = 0.0;
   long long stage_launches_first = 0, stage_launches_later = 0;
@@ -136,6 +147,9 @@ void set_rhs(pdg_ctx* c, const double* rhs, bool on_device);
 void step_lserk(pdg_ctx* c, double dt, int nsteps);
 /// nsteps AB3 steps with the LSERK bootstrap of TimeStepper::step (solver.cpp:559-581)
 void step_ab3(pdg_ctx* c, double dt, int nsteps);
+/// nmacro multi-rate AB3 macro steps (2^L fine steps of dt each); the first two
+/// macro steps after set_state are the LSERK45 bootstrap at dt
+void step_mrab(pdg_ctx* c, double dt, int nmacro);
 double energy(pdg_ctx* c);
 long long check_finite(pdg_ctx* c);
 void synchronize(pdg_ctx* c);

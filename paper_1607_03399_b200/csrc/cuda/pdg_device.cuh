@@ -195,6 +195,12 @@ cudaError_t launch_gather_values(const long long* idx, long long n, const double
 cudaError_t launch_scatter_values(const long long* idx, long long n, const double* buf, double* u, cudaStream_t s);
 cudaError_t launch_ab3_update(long long n, double* u, const double* f0, const double* f1, const double* f2,
                               double dt, cudaStream_t s);
+/// multi-rate AB3 update of one rate level (DOF ranges [w0,w1) and [t0,t1));
+/// commit = end of the level's step (the AB3 formula, u0 <- u), else the
+/// predictor at theta in (0,1) of the step
+cudaError_t launch_mrab_update(long long w0, long long w1, long long t0, long long t1, double* u, double* u0,
+                               const double* f0, const double* f1, const double* f2, double h, double theta,
+                               int commit, cudaStream_t s);
 cudaError_t launch_to_device_layout(int N, long long Kw, long long Kt, const int* dev_to_ref,
                                     const long long* ref_offset, const double* src_ref,
                                     double* dst_dev, cudaStream_t s);

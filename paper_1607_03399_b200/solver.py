@@ -385,9 +385,10 @@ class DeviceContext:
         return out
 
     def step(self, dt, nsteps=1, t=0.0, integrator="lserk4"):
-        """TimeStepper::step x nsteps on the resident state (lserk4 or ab3, solver.cpp:536-581)."""
+        """TimeStepper::step x nsteps on the resident state (lserk4 or ab3, solver.cpp:536-581);
+        integrator="mrab": nsteps multi-rate AB3 macro steps of fine step dt."""
         tt = C.c_double(t)
-        fn = lib().pdg_step_ab3 if integrator == "ab3" else lib().pdg_step_lserk
+        fn = {"ab3": lib().pdg_step_ab3, "mrab": lib().pdg_step_mrab}.get(integrator, lib().pdg_step_lserk)
         check(fn(self._h, dt, nsteps, C.byref(tt)))
         return tt.value
 
@@ -417,6 +418,13 @@ class DeviceContext:
         wb, tb = C.c_double(), C.c_double()
         check(lib().pdg_stage_bytes(self._h, C.byref(wb), C.byref(tb)))
         return wb.value, tb.value
+
+    def mrab_levels(self):
+        """(rate level of every reference element, number of levels)"""
+        lev = np.zeros(self.disc.num_elements(), dtype=np.int32)
+        n = C.c_int()
+        check(lib().pdg_mrab_levels(self._h, _ip(lev), C.byref(n)))
+        return lev, n.value
 
     def launch_info(self):
         """last wedge / tet stage launch: {launched, teams, tickets, per_ticket} each"""
@@ -483,9 +491,10 @@ class RunOptions:
     energy_interval: float = 0.0
     watchdog_every: int = 50
     blowup_factor: float = 10.0
-    integrator: str = "lserk4"  # IntegratorKind: "lserk4" | "ab3"
+    integrator: str = "lserk4"  # IntegratorKind: "lserk4" | "ab3" | "mrab" (context with multi-rate levels)
     snapshot_interval: float = 0.0  # 0: no snapshots
     snapshot_cb: object = None  # callable(u: np.ndarray (copy), time: float, index: int)
+    mrab_levels: int = 3  # integrator="mrab": up to this many extra rate levels (PDG_CTX_MRAB_LEVELS)
 
 
 @dataclass
@@ -512,14 +521,15 @@ def run_simulation(disc: Discretization, state: SolutionState, opts: RunOptions,
     else:
         cb = capi.SNAPSHOT_CB()
     o = capi.RunOptions(opts.final_time, opts.cfl, opts.fixed_dt, opts.energy_interval,
-                        opts.watchdog_every, opts.blowup_factor, 1 if opts.integrator == "ab3" else 0,
+                        opts.watchdog_every, opts.blowup_factor, {"ab3": 1, "mrab": 2}.get(opts.integrator, 0),
                         opts.snapshot_interval, cb, None)
     r = capi.RunResult()
     log = np.zeros(2 * max_log)
     t = C.c_double(state.time)
     state.u = np.ascontiguousarray(state.u, dtype=np.float64)
     try:
-        check(lib().pdg_run_simulation(disc.device().handle, _dp(state.u), C.byref(t), C.byref(o), C.byref(r),
+        flags = capi.CTX_MRAB_LEVELS(opts.mrab_levels) if opts.integrator == "mrab" else 0
+        check(lib().pdg_run_simulation(disc.device(flags=flags).handle, _dp(state.u), C.byref(t), C.byref(o), C.byref(r),
                                        _dp(log), max_log))
     finally:
         state.time = t.value  # on a watchdog failure: the failure time, like the reference

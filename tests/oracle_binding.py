@@ -38,6 +38,7 @@ def lib():
         h.orc_lserk.argtypes = [vp, dp, C.c_double, C.c_int, C.c_int, C.c_int]
         h.orc_energy.argtypes = [vp, dp, C.c_int, dp]
         h.orc_ab3.argtypes = [vp, dp, C.c_double, C.c_int, C.c_int]
+        h.orc_mrab.argtypes = [vp, dp, C.POINTER(C.c_int), C.c_int, C.c_double, C.c_int, C.c_int]
         h.orc_run.argtypes = [vp, dp, dp, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int, dp]
         h.orc_gll_newton.argtypes = [C.c_int, dp, dp]
         ip = C.POINTER(C.c_int)
@@ -83,6 +84,14 @@ def lserk(disc, u, dt, nsteps, threads=4, parallel_update=True):
 def ab3(disc, u, dt, nsteps, threads=4):
     u = np.array(u, dtype=np.float64, copy=True)
     _ok(lib().orc_ab3(disc.handle, _dp(u), dt, nsteps, threads))
+    return u
+
+
+def mrab(disc, u, level, nlev, dt, nmacro, threads=4):
+    """multi-rate AB3 (pdg_step_mrab's algorithm): level[e] = rate level of element e"""
+    u = np.array(u, dtype=np.float64, copy=True)
+    lev = np.ascontiguousarray(level, dtype=np.int32)
+    _ok(lib().orc_mrab(disc.handle, _dp(u), lev.ctypes.data_as(C.POINTER(C.c_int)), nlev, dt, nmacro, threads))
     return u
 
 
