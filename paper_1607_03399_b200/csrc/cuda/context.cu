@@ -18,6 +18,10 @@
 
 using prismdg::DeviceError;
 
+#ifndef PDG_WEDGE_WS_DEFAULT
+#define PDG_WEDGE_WS_DEFAULT 0
+#endif
+
 namespace pdg {
 
 namespace {
@@ -131,6 +135,16 @@ int dev_node_of(const prismdg::Discretization& d, bool wedge, int nref) {
   return j * nts_of(d.degree) + i; // device slice stride (padded at N = 5)
 }
 
+// exact-mode wedge kernel for N >= 4: the warp-specialised one (wedge_ws.cu)
+// unless PDG_WEDGE_WS=0 selects the single-role DMMA kernel (wedge_dmma.cu)
+bool use_wedge_ws(int N) {
+  static const int env = [] {
+    const char* v = std::getenv("PDG_WEDGE_WS");
+    return v ? std::atoi(v) : -1;
+  }();
+  return wedge_ws_supported(N) && env != 0 && (env > 0 || PDG_WEDGE_WS_DEFAULT);
+}
+
 void launch_checked(pdg_ctx* c, const StageParams& p0, bool wedge) {
   cudaEvent_t a = nullptr, b = nullptr;
   if (c->flags & 2) {
@@ -145,7 +159,8 @@ void launch_checked(pdg_ctx* c, const StageParams& p0, bool wedge) {
                     : c->wadg ? (c->N <= wedge_wadg_simt_max_degree() ? launch_wedge_wadg_simt_stage(c->N, p, c->stream)
                                                                      : launch_wedge_wadg_stage(c->N, p, c->stream))
                     : c->wedge_simt ? launch_wedge_simt_stage(c->N, p, c->stream)
-                                    : launch_wedge_stage(c->N, p, c->stream);
+                    : use_wedge_ws(c->N) ? launch_wedge_ws_stage(c->N, p, c->stream)
+                                         : launch_wedge_stage(c->N, p, c->stream);
   if (err != cudaSuccess) {
     if (a) cudaEventDestroy(a);
     if (b) cudaEventDestroy(b);

@@ -173,6 +173,9 @@ struct EnergyParams {
 // launchers (instantiated per degree in the .cu files)
 cudaError_t launch_wedge_stage(int N, const StageParams& p, cudaStream_t s); // FP64 tensor-core (DMMA) kernel
 cudaError_t launch_tet_stage(int N, const StageParams& p, cudaStream_t s);
+/// warp-specialised wedge kernel (producer warp: tickets, TMA, gathers, fluxes; N = 4..7)
+bool wedge_ws_supported(int N);
+cudaError_t launch_wedge_ws_stage(int N, const StageParams& p, cudaStream_t s);
 bool tet_dmma_supported(int N);
 int wedge_simt_max_degree();
 cudaError_t launch_wedge_simt_stage(int N, const StageParams& p, cudaStream_t s); // low-order CUDA-core wedge kernel
