@@ -15,14 +15,20 @@
 // barriers that the flux phase's imbalance feeds; here the compute warps never
 // touch global gathers and meet only one named barrier per element (V).
 //
-// Synchronisation per team (mbarriers in shared memory, parity by element):
-//   full[s]  : TMA bytes of stage s landed (producer lane 0 arrive.expect_tx)
-//   ffull[s] : fluxes of the element in stage s written (32 producer lanes)
-//   done[s]  : compute warps finished the element in stage s (32 T lanes);
-//              the producer refills stage s (and its flux set) after it.
-// The element id travels with the stage (elem[s], written before the TMA is
+// Stages: an element's bytes arrive in two bulk-copy groups, A = state +
+// record + connectivity (read by both roles; ring of 3) and B = residual +
+// L^{tri,k} + quad lifts (compute warps only; ring of 2).  When the compute
+// warps finish element n-1 the producer issues A(n+2) and B(n+1), so the
+// fluxes of element n+1 (whose A copy landed an element earlier) are computed
+// during element n: only the neighbour gathers' L2 latency is on the
+// producer's path, hidden behind a whole element of compute.
+// Synchronisation per team (mbarriers in shared memory):
+//   fullA[n%3], fullB[n&1] : the copies of element n landed
+//   ffull[n&1]             : fluxes of element n written (32 producer lanes)
+//   done[n&1]              : compute warps finished element n (32 T lanes)
+// Element ids travel with the A slot (elem[n%3], written before the copy is
 // issued; the arrive's release / the wait's acquire order it).  A ticket past
-// the end is published as elem[s] >= Kw_active with a plain arrive: both roles
+// the end is published as elem >= Kw_active with a plain arrive: both roles
 // leave their loops on it.
 #include <cuda_runtime.h>
 
@@ -51,6 +57,11 @@ constexpr int kComboCap = 4096; // ints of neighbour node maps kept in shared me
 #ifndef PDG_WS_GATHER_BATCH
 #define PDG_WS_GATHER_BATCH 5
 #endif
+// the producer also forms V (the vertical products G1 + the folded bottom/top
+// pressure lifts) for every row tile, so the compute warps need no barrier at all
+#ifndef PDG_WS_PRODUCER_V
+#define PDG_WS_PRODUCER_V 1
+#endif
 
 template <int N>
 struct WCfg {
@@ -61,7 +72,8 @@ struct WCfg {
   static constexpr int WPT = T + 1;   // + the producer warp
   static constexpr int LF = lcomp_of(N), QF = qcomp_of(N);
   static constexpr int USTR = r4(4 * NP) + 2;
-  static constexpr int STAGE = r2(2 * USTR + LF + QF + WG + kWC / 2);
+  static constexpr int STA = r2(USTR + WG + kWC / 2); // A: state, record, connectivity
+  static constexpr int STB = r2(USTR + LF + QF);      // B: residual, L, quad lifts
   static constexpr bool KP = (NT & 1) && ST == NT;
   static constexpr int VST = KP ? NT : cf_stride(NT);
   static constexpr int VS = r2((NPJ - 1) * VST + 4 * KS + 8);
@@ -69,8 +81,8 @@ struct WCfg {
   static constexpr int FTRI = r2(4 * KS + NT + 8);
   static constexpr int ZS = r2(4 * KS);
   static constexpr int FB = 2 * (FTRI + FQ);
-  static constexpr int HDR = 8; // 6 mbarriers + elem[2]
-  static constexpr int PER_TEAM = HDR + 2 * STAGE + 2 * VS + 2 * FB + ZS;
+  static constexpr int HDR = 12; // 9 mbarriers + elem[3]
+  static constexpr int PER_TEAM = HDR + 3 * STA + 2 * STB + 2 * VS + 2 * FB + ZS;
   static constexpr int TABLES = r2(2 * IT * KS * 32 + JT * KT * 32 + 2 * NQ + ceil_div(FW, 2) + kComboCap / 2);
   static constexpr int SMEM_BUDGET = 225 * 1024;
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
@@ -101,24 +113,27 @@ __device__ __forceinline__ void named_sync(int id, int nthreads) {
 }
 
 template <int N>
-__device__ __forceinline__ void ws_load_element(const StageParams& p, double* stg, long long e, const double* res_src,
-                                                uint64_t* bar) {
+__device__ __forceinline__ void ws_load_a(const StageParams& p, double* sa, long long e, uint64_t* bar) {
   using C = WCfg<N>;
   constexpr int NP = C::NP;
-  double* U = stg;
-  double* R = U + C::USTR;
-  double* L = R + C::USTR;
-  double* Q = L + C::LF;
-  double* G = Q + C::QF;
-  const uint32_t bytes = 8u * (4 * NP + C::LF + C::QF + C::WG) + 4u * kWC + (res_src ? 32u * NP : 0u);
+  // the state stays in L2 for the neighbours' trace gathers; the rest is touched once
   const uint64_t keep = l2_policy_evict_last(), stream = l2_policy_evict_first();
-  mbar_arrive_expect_tx(bar, bytes);
-  tma_load_1d_hint(U, p.u_in + e * 4 * NP, 32 * NP, bar, keep);
-  if (res_src) tma_load_1d_hint(R, res_src + e * 4 * NP, 32 * NP, bar, stream);
-  tma_load_1d_hint(L, p.Lt + e * C::LF, 8 * C::LF, bar, stream);
-  tma_load_1d_hint(Q, p.QL + e * C::QF, 8 * C::QF, bar, stream);
-  tma_load_1d_hint(G, p.wgeo + e * C::WG, 8 * C::WG, bar, stream);
-  tma_load_1d_hint(G + C::WG, p.wconn + e * kWC, 4 * kWC, bar, stream);
+  mbar_arrive_expect_tx(bar, 8u * (4 * NP + C::WG) + 4u * kWC);
+  tma_load_1d_hint(sa, p.u_in + e * 4 * NP, 32 * NP, bar, keep);
+  tma_load_1d_hint(sa + C::USTR, p.wgeo + e * C::WG, 8 * C::WG, bar, stream);
+  tma_load_1d_hint(sa + C::USTR + C::WG, p.wconn + e * kWC, 4 * kWC, bar, stream);
+}
+
+template <int N>
+__device__ __forceinline__ void ws_load_b(const StageParams& p, double* sb, long long e, const double* res_src,
+                                          uint64_t* bar) {
+  using C = WCfg<N>;
+  constexpr int NP = C::NP;
+  const uint64_t stream = l2_policy_evict_first();
+  mbar_arrive_expect_tx(bar, 8u * (C::LF + C::QF) + (res_src ? 32u * NP : 0u));
+  if (res_src) tma_load_1d_hint(sb, res_src + e * 4 * NP, 32 * NP, bar, stream);
+  tma_load_1d_hint(sb + C::USTR, p.Lt + e * C::LF, 8 * C::LF, bar, stream);
+  tma_load_1d_hint(sb + C::USTR + C::LF, p.QL + e * C::QF, 8 * C::QF, bar, stream);
 }
 
 template <int N, bool COMBO_SMEM, bool FUSED>
@@ -159,17 +174,20 @@ __global__ void __launch_bounds__(WCfg<N>::THREADS, 1) wedge_ws_kernel(const Sta
   const int tw = (threadIdx.x >> 5) - team * C::WPT; // warp within team: < T compute, == T producer
   const int lane = threadIdx.x & 31;
   double* tbase = smem + C::TABLES + (size_t)team * C::PER_TEAM;
-  uint64_t* full = reinterpret_cast<uint64_t*>(tbase);
-  uint64_t* ffull = full + 2;
-  uint64_t* done = full + 4;
-  volatile long long* elem = reinterpret_cast<volatile long long*>(full + 6);
-  double* stg0 = tbase + C::HDR;
-  double* V0 = stg0 + 2 * C::STAGE;
+  uint64_t* fullA = reinterpret_cast<uint64_t*>(tbase);
+  uint64_t* fullB = fullA + 3;
+  uint64_t* ffull = fullA + 5;
+  uint64_t* done = fullA + 7;
+  volatile long long* elem = reinterpret_cast<volatile long long*>(fullA + 9);
+  double* sA0 = tbase + C::HDR;
+  double* sB0 = sA0 + 3 * C::STA;
+  double* V0 = sB0 + 2 * C::STB;
   double* F0 = V0 + 2 * C::VS;
   const double* Zero = F0 + 2 * C::FB; // ZS zeros, never written
   if (tw == T && lane == 0) {
+    for (int s = 0; s < 3; ++s) mbar_init(fullA + s, 1);
     for (int s = 0; s < 2; ++s) {
-      mbar_init(full + s, 1);
+      mbar_init(fullB + s, 1);
       mbar_init(ffull + s, 32);
       mbar_init(done + s, 32 * T);
     }
@@ -194,24 +212,36 @@ __global__ void __launch_bounds__(WCfg<N>::THREADS, 1) wedge_ws_kernel(const Sta
       }
       return bnext++;
     };
-    auto issue = [&](int s) { // lane 0
+    auto issue_a = [&](int n) { // lane 0: grab element n, copy its A group
       const long long e = grab();
-      elem[s] = e;
+      const int a = n % 3;
+      elem[a] = e;
       if (e < p.Kw_active) {
         fence_proxy_async_smem();
-        ws_load_element<N>(p, stg0 + s * C::STAGE, e, res_src, full + s);
+        ws_load_a<N>(p, sA0 + a * C::STA, e, fullA + a);
       } else {
-        mbar_arrive(full + s);
+        mbar_arrive(fullA + a);
       }
     };
-    if (lane == 0) issue(0);
+    auto issue_b = [&](int n) { // lane 0: the B group of element n (already grabbed)
+      const long long e = elem[n % 3];
+      if (e < p.Kw_active) {
+        fence_proxy_async_smem();
+        ws_load_b<N>(p, sB0 + (n & 1) * C::STB, e, res_src, fullB + (n & 1));
+      }
+    };
+    if (lane == 0) {
+      issue_a(0);
+      issue_a(1);
+      issue_b(0);
+    }
     for (int n = 0;; ++n) {
-      const int s = n & 1;
-      mbar_wait(full + s, (n >> 1) & 1);
-      if (elem[s] >= p.Kw_active) break;
+      const int s = n & 1, a = n % 3;
+      mbar_wait(fullA + a, (n / 3) & 1);
+      if (elem[a] >= p.Kw_active) break;
       if (surf) {
-        const double* U = stg0 + s * C::STAGE;
-        const double* G = U + 2 * C::USTR + C::LF + C::QF;
+        const double* U = sA0 + a * C::STA;
+        const double* G = U + C::USTR;
         const int* Cn = reinterpret_cast<const int*>(G + WG);
         double* Ftp = F0 + s * C::FB; // tri-face fluxes: p part [2][NT]
         double* Ftu = Ftp + C::FTRI;  //                  u part
@@ -284,11 +314,50 @@ __global__ void __launch_bounds__(WCfg<N>::THREADS, 1) wedge_ws_kernel(const Sta
           }
         }
       }
+      if (PDG_WS_PRODUCER_V) {
+        // V[j][i] of every row tile (G1 of wedge_dmma.cu), parity buffer s
+        __syncwarp(); // the tri-face fluxes of all lanes are in shared memory
+        const double* U = sA0 + a * C::STA;
+        const double* G = U + C::USTR;
+        const double* Ftp = F0 + s * C::FB;
+        double* V = V0 + s * C::VS;
+        const int gid = lane >> 2, tig = lane & 3;
+        const double tzJ = G[W_TZJ], jfb = G[W_JFB], jft = G[W_JFT];
+#pragma unroll
+        for (int t = 0; t < C::IT; ++t) {
+          const int i = 8 * t + gid;
+          const double fb = surf ? jfb * Ftp[i] : 0.0, ftop = surf ? jft * Ftp[NT + i] : 0.0;
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) {
+            double d[2] = {0.0, 0.0};
+            if (vol) {
+              const int jb = 8 * jt + gid;
+              const int jc = jb < NQ ? jb : NQ - 1;
+              const double sx_ = G[W_TXJ + jc], sy_ = G[w_tyj(N) + jc];
+#pragma unroll
+              for (int s2 = 0; s2 < KT; ++s2) {
+                const int l = 4 * s2 + tig;
+                const double bd = sDt[((jt * KT + s2) << 5) + lane];
+                dmma(d, U[(NQ + l) * ST + i], sx_ * bd);
+                dmma(d, U[(2 * NQ + l) * ST + i], sy_ * bd);
+                dmma(d, U[(3 * NQ + l) * ST + i], tzJ * bd);
+              }
+            }
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              const int j = 8 * jt + 2 * tig + c;
+              if (i < NT && j < NQ) V[j * VST + i] = -d[c] + fb * sProf[j] + ftop * sProf[NQ + j];
+            }
+          }
+        }
+      }
       mbar_arrive(ffull + s);
-      // refill the other stage (element n-1's) with element n+1 once the compute
-      // warps are done with element n-1
+      // element n-1 done: its A slot takes element n+2, its B slot element n+1
       if (n >= 1) mbar_wait(done + (s ^ 1), ((n - 1) >> 1) & 1);
-      if (lane == 0) issue(s ^ 1);
+      if (lane == 0) {
+        issue_a(n + 2);
+        issue_b(n + 1);
+      }
       __syncwarp();
     }
     return;
@@ -298,26 +367,28 @@ __global__ void __launch_bounds__(WCfg<N>::THREADS, 1) wedge_ws_kernel(const Sta
   const int w = tw, gid = lane >> 2, tig = lane & 3;
   const int bar_id = 1 + team;
   for (int n = 0;; ++n) {
-    const int s = n & 1, ph = (n >> 1) & 1;
-    mbar_wait(full + s, ph);
-    const long long e = elem[s];
+    const int s = n & 1, ph = (n >> 1) & 1, a = n % 3;
+    mbar_wait(fullA + a, (n / 3) & 1);
+    const long long e = elem[a];
     if (e >= p.Kw_active) break;
-    const double* U = stg0 + s * C::STAGE;
-    const double* R = U + C::USTR;
+    const double* U = sA0 + a * C::STA;
+    const double* G = U + C::USTR;
+    const double* R = sB0 + s * C::STB;
     const double* Lf = R + C::USTR;
     const double* Qf = Lf + C::LF;
-    const double* G = Qf + C::QF;
     const double* Ftp = F0 + s * C::FB;
     const double* Ftu = Ftp + C::FTRI;
     const double* Fqp = Ftu + C::FTRI;
     const double* Fqu = Fqp + C::FQ;
-    double* V = V0 + (n & 1) * C::VS;
+    double* V = V0 + s * C::VS;
     const double* Us = U; // state, slice stride ST
     constexpr int SP = ST;
+    mbar_wait(fullB + s, ph);
     mbar_wait(ffull + s, ph);
 
     // ---- G1: V[j][i] for row tile w, with the bottom/top pressure lifts folded in
-    {
+    // (formed by the producer when PDG_WS_PRODUCER_V)
+    if (!PDG_WS_PRODUCER_V) {
       const int i = 8 * w + gid;
       const double tzJ = G[W_TZJ], jfb = G[W_JFB], jft = G[W_JFT];
       const double fb = surf ? jfb * Ftp[i] : 0.0, ftop = surf ? jft * Ftp[NT + i] : 0.0;
@@ -344,7 +415,7 @@ __global__ void __launch_bounds__(WCfg<N>::THREADS, 1) wedge_ws_kernel(const Sta
         }
       }
     }
-    named_sync(bar_id, 32 * T);
+    if (!PDG_WS_PRODUCER_V) named_sync(bar_id, 32 * T);
 
     // ---- row tile w: G2, G3, G4, G5 and the epilogue ---------------------------
     {
@@ -490,7 +561,7 @@ __global__ void __launch_bounds__(WCfg<N>::THREADS, 1) wedge_ws_kernel(const Sta
           }
         }
     }
-    // stage s, its flux set and (two elements on) this V buffer may be reused
+    // this element's A and B slots and its flux set may be reused
     mbar_arrive(done + s);
   }
 }
@@ -520,7 +591,9 @@ cudaError_t launch_ws_NC(const StageParams& p, cudaStream_t s) {
   q.ticket_base = *p.ticket_host_next;
   q.ticket_batch = ws_ticket_batch(N);
   const unsigned long long B = (unsigned long long)q.ticket_batch;
-  *p.ticket_host_next += B * (((unsigned long long)nact + B - 1) / B + (unsigned long long)grid * C::TPB);
+  // every team's producer grabs two tickets past the end (it runs two elements
+  // ahead), so the counter ends exactly here and the next launch starts clean
+  *p.ticket_host_next += B * (((unsigned long long)nact + B - 1) / B + 2ull * (unsigned long long)grid * C::TPB);
   kern<<<grid, C::THREADS, C::SMEM_BYTES, s>>>(q);
   if (p.info) *p.info = LaunchInfo{1, (long long)grid * C::TPB, (nact + (long long)B - 1) / (long long)B, (int)B};
   return cudaGetLastError();
