@@ -102,6 +102,15 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #define PDG_REG_OPS_MAXN 0
 #endif
 
+// per-element serial work spread over the team (N <= 5, no-end-barrier schedule):
+// the ticket grab moves to the last warp (the one with the fewest flux tasks)
+// and each warp issues its share of the element's bulk copies after the flux
+// barrier (one arrive.expect_tx per warp), instead of warp 0 doing both while
+// the others wait at the next team barrier
+#ifndef PDG_SPLIT_ISSUE
+#define PDG_SPLIT_ISSUE 0
+#endif
+
 /// k index of lane column tig in k-step s (see PDG_KPERM)
 __host__ __device__ constexpr int kmap(int s, int tig, int KS, bool perm) {
   return (perm && s < 4 * (KS / 4)) ? 16 * (s >> 2) + 4 * tig + (s & 3) : 4 * s + tig;
@@ -204,6 +213,42 @@ __device__ __forceinline__ void load_element(const StageParams& p, double* stg, 
   tma_load_1d_hint(G + C::WG, p.wconn + e * kWC, 4 * kWC, bar, stream);
 }
 
+/// warp `part` of T issues copies c = part, part + T, ... of the element's
+/// state / residual / L / quad lifts / record / connectivity, with its own
+/// arrive.expect_tx (the barrier counts T arrivals)
+template <int N, int NST>
+__device__ __forceinline__ void load_element_part(const StageParams& p, double* stg, long long e,
+                                                  const double* res_src, uint64_t* bar, int part) {
+  constexpr int T = DCfg<N, NST>::T;
+  using C = DCfg<N, NST>;
+  constexpr int NP = C::NP;
+  double* U = stg;
+  double* R = U + C::USTR;
+  double* L = R + C::USTR;
+  double* Q = L + C::LF;
+  double* G = Q + C::QF;
+  auto size_of = [&](int c) -> uint32_t {
+    return c == 0 ? 32u * NP : c == 1 ? (res_src ? 32u * NP : 0u) : c == 2 ? 8u * C::LF
+         : c == 3 ? 8u * C::QF : c == 4 ? 8u * C::WG : 4u * kWC;
+  };
+  uint32_t bytes = 0;
+#pragma unroll
+  for (int c = 0; c < 6; ++c)
+    if (c % T == part) bytes += size_of(c);
+  const uint64_t keep = l2_policy_evict_last(), stream = l2_policy_evict_first();
+  mbar_arrive_expect_tx(bar, bytes);
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    if (c % T != part) continue;
+    if (c == 0) tma_load_1d_hint(U, p.u_in + e * 4 * NP, size_of(0), bar, keep);
+    if (c == 1 && res_src) tma_load_1d_hint(R, res_src + e * 4 * NP, size_of(1), bar, stream);
+    if (c == 2) tma_load_1d_hint(L, p.Lt + e * C::LF, size_of(2), bar, stream);
+    if (c == 3) tma_load_1d_hint(Q, p.QL + e * C::QF, size_of(3), bar, stream);
+    if (c == 4) tma_load_1d_hint(G, p.wgeo + e * C::WG, size_of(4), bar, stream);
+    if (c == 5) tma_load_1d_hint(G + C::WG, p.wconn + e * kWC, size_of(5), bar, stream);
+  }
+}
+
 template <int N, bool COMBO_SMEM, bool FUSED, int NST>
 __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(const StageParams p) {
   using C = DCfg<N, NST>;
@@ -252,9 +297,11 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
   const double* Zero = Fbase + C::FBUF * C::FB; // ZS zeros, never written
   double* Upad = Fbase + C::FBUF * C::FB + C::ZS; // padded state copy (C::PAD)
   constexpr int SP = C::SP;
+  constexpr bool SPLIT = PDG_SPLIT_ISSUE && C::NOEND;
+  const bool grabber = SPLIT ? tt == 32 * (T - 1) : tt == 0; // thread that owns the ticket state
   if (tt == 0) {
-    mbar_init(bar, 1);
-    mbar_init(bar + 1, 1);
+    mbar_init(bar, SPLIT ? T : 1);
+    mbar_init(bar + 1, SPLIT ? T : 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -316,13 +363,14 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
     }
     return bnext++;
   };
-  if (tt == 0) {
+  if (grabber) {
     const long long e0 = grab();
     slot[0] = e0;
-    if (e0 < p.Kw_active) load_element<N, NST>(p, stg0, e0, res_src, bar);
+    if (!SPLIT && e0 < p.Kw_active) load_element<N, NST>(p, stg0, e0, res_src, bar);
   }
   team_sync(bar_id, 32 * T);
   long long e = slot[0];
+  if (SPLIT && lane == 0 && e < p.Kw_active) load_element_part<N, NST>(p, stg0, e, res_src, bar, w);
 
   // neighbour traces of this thread's face-node tasks (prefetching the next
   // element's during this element's products was measured slower: it exposes
@@ -358,7 +406,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
   for (int n = 0; e < p.Kw_active; ++n) {
     const int s = NST == 2 ? (n & 1) : 0;
     long long en = 0;
-    if (tt == 0) {
+    if (grabber) {
       en = grab();
       slot[1 + (n & 1)] = en; // parity slots: rewritten only after every thread read it
     }
@@ -465,9 +513,16 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
     }
     team_sync(bar_id, 32 * T);
     // every warp of the team has left the previous element: its stage may be refilled
-    if (C::NOEND && tt == 0 && en < p.Kw_active) {
+    if (C::NOEND && !SPLIT && tt == 0 && en < p.Kw_active) {
       fence_proxy_async_smem();
       load_element<N, NST>(p, stg0 + (s ^ 1) * C::STAGE, en, res_src, bar + (s ^ 1));
+    }
+    if (SPLIT && lane == 0) {
+      const long long enx = slot[1 + (n & 1)]; // written before the flux barrier by the grabber
+      if (enx < p.Kw_active) {
+        fence_proxy_async_smem();
+        load_element_part<N, NST>(p, stg0 + (s ^ 1) * C::STAGE, enx, res_src, bar + (s ^ 1), w);
+      }
     }
 
     // ---- G1: V[j][i] for row tile w, with the bottom/top pressure lifts folded in
