@@ -506,6 +506,7 @@ def main():
         # communicator setup lines (rank count, NVLS / P2P transport) on stderr
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # keep stdout to the one JSON line
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks = load_peaks()
     if use_dist:
