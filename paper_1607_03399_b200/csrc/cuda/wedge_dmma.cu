@@ -111,6 +111,14 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #define PDG_SPLIT_ISSUE 0
 #endif
 
+// when a ticket (a batch of consecutive elements) is grabbed, prefetch the
+// whole batch's streamed arrays into L2 (cp.async.bulk.prefetch.L2): the
+// elements after the next one get their HBM reads in flight early, without
+// shared memory or registers, so more bytes are in flight per SM
+#ifndef PDG_L2_PREFETCH
+#define PDG_L2_PREFETCH 0
+#endif
+
 /// k index of lane column tig in k-step s (see PDG_KPERM)
 __host__ __device__ constexpr int kmap(int s, int tig, int KS, bool perm) {
   return (perm && s < 4 * (KS / 4)) ? 16 * (s >> 2) + 4 * tig + (s & 3) : 4 * s + tig;
@@ -360,6 +368,15 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
     if (bnext >= bend) {
       bnext = p.Kw_begin + (long long)(atomicAdd(p.ticket, (unsigned long long)B) - p.ticket_base);
       bend = bnext + B < p.Kw_active ? bnext + B : (bnext < p.Kw_active ? p.Kw_active : bnext + 1);
+      if (PDG_L2_PREFETCH && bnext < p.Kw_active) {
+        // the batch [bnext, bend) is contiguous in every streamed array
+        const long long nb = bend - bnext;
+        prefetch_l2_bulk(p.u_in + bnext * 4 * NP, (uint32_t)(nb * 32 * NP));
+        if (res_src) prefetch_l2_bulk(res_src + bnext * 4 * NP, (uint32_t)(nb * 32 * NP));
+        prefetch_l2_bulk(p.Lt + bnext * C::LF, (uint32_t)(nb * 8 * C::LF));
+        prefetch_l2_bulk(p.QL + bnext * C::QF, (uint32_t)(nb * 8 * C::QF));
+        prefetch_l2_bulk(p.wgeo + bnext * C::WG, (uint32_t)(nb * 8 * C::WG));
+      }
     }
     return bnext++;
   };
