@@ -442,7 +442,7 @@ def relaunch(args):
     torch.distributed.run with the same arguments; refuse when fewer than N
     GPUs are visible (NCCL cannot put two ranks on one device)."""
     import socket
-    if args.impl == "ours":
+    if args.impl == "ours" and not args.launch_check:
         import torch
         have = torch.cuda.device_count()
         if have < args.gpus:
@@ -481,6 +481,8 @@ def main():
                     help="run the multi-GPU path (slab partition, DistributedLSERK, NCCL group) even at one GPU")
     ap.add_argument("--mass", default="exact", choices=["exact", "wadg"],
                     help="exact stored-lift mass (reference parity mode) or weight-adjusted (north-star WADG)")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="test hook: relaunch as for --gpus N, then every rank reports its rank and exits")
     args = ap.parse_args()
     args.sublayers = [int(x) for x in args.sublayers.split(",")]
     args.warmup = max(3, args.warmup)
@@ -491,6 +493,10 @@ def main():
     if "WORLD_SIZE" in os.environ and ws != args.gpus and args.gpus > 1:
         print(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}", file=sys.stderr, flush=True)
         return 3
+    if args.launch_check:
+        print(json.dumps({"rank": rank, "world_size": ws, "local_rank": local,
+                          "master": os.environ.get("MASTER_ADDR")}), flush=True)
+        return 0
     if args.impl == "reference":
         return run_reference_arm(args)
 

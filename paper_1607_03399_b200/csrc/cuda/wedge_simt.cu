@@ -30,6 +30,7 @@
 #include <cstdlib>
 
 #include "pdg_device.cuh"
+#include "tma.cuh"
 
 namespace pdg {
 
@@ -104,6 +105,13 @@ __host__ __device__ constexpr int slot_stride(int x, int NT, int H) {
 // the WADG variant has no slice split: min 3 CTAs/SM at N = 1 (4 spills), 1 above
 #ifndef PDG_WADG_SIMT_MINB
 #define PDG_WADG_SIMT_MINB(N) ((N) == 1 ? 3 : 1)
+#endif
+
+// prefetch the streamed arrays of the chunk two tickets ahead into L2 when its
+// ticket is grabbed (cp.async.bulk.prefetch.L2), so its cp.async copies and
+// the per-thread operand loads hit L2 and more HBM bytes are in flight
+#ifndef PDG_SIMT_L2_PREFETCH
+#define PDG_SIMT_L2_PREFETCH 0
 #endif
 
 template <int N, bool WADG = false>
@@ -259,7 +267,21 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, WADG ? PDG_WADG_SIMT_M
     }
     // next ticket; the slot alternates with the iteration parity so it is never
     // rewritten before every thread has read it
-    if (threadIdx.x == 0) slot[2 + (it & 1)] = (long long)(atomicAdd(p.ticket, 1ULL) - p.ticket_base);
+    if (threadIdx.x == 0) {
+      const long long cf = (long long)(atomicAdd(p.ticket, 1ULL) - p.ticket_base);
+      slot[2 + (it & 1)] = cf;
+      if (PDG_SIMT_L2_PREFETCH && cf < nchunk) {
+        const long long f0 = p.Kw_begin + cf * E;
+        const long long nf = nel_of(cf);
+        prefetch_l2_bulk(p.u_in + f0 * 4 * NP, (uint32_t)(nf * 32 * NP));
+        if (res_src) prefetch_l2_bulk(res_src + f0 * 4 * NP, (uint32_t)(nf * 32 * NP));
+        if (!WADG) {
+          prefetch_l2_bulk(p.Lt + f0 * lcomp_of(N), (uint32_t)(nf * 8 * lcomp_of(N)));
+          prefetch_l2_bulk(p.QL + f0 * qcomp_of(N), (uint32_t)(nf * 8 * qcomp_of(N)));
+        }
+        prefetch_l2_bulk(p.wgeo + f0 * WG, (uint32_t)(nf * 8 * WG));
+      }
+    }
     __syncthreads();
     // every thread has left the previous chunk: its stage takes the next one
     if (C::NOEND) {

@@ -98,3 +98,18 @@ def test_strong_partition_covers_the_single_domain_mesh():
     for p in parts:
         for q, ids in p.send.items():
             assert np.array_equal(p.local_to_global[ids], parts[q].local_to_global[parts[q].recv[p.rank]])
+
+
+def test_multi_gpu_bench_spawns_one_rank_per_gpu():
+    """--gpus 2 outside torchrun re-launches bench.py under torch.distributed.run
+    with two ranks (127.0.0.1 rendezvous); --launch-check makes each rank report
+    itself instead of touching a GPU."""
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launch-check"],
+                         capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert sorted(l["rank"] for l in lines) == [0, 1]
+    assert all(l["world_size"] == 2 and l["master"] == "127.0.0.1" for l in lines)
