@@ -340,7 +340,29 @@ def measure_degree(args, degree, ws, rank, local, peaks, with_e2e=True):
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             el = float(t.item())
         res["e2e"] = {"value": dofs * e2e_steps * ws / el, "unit": UNIT, "h2d_bytes_per_step": dofs * 8,
-                      "d2h_bytes_per_step": dofs * 8, "steps": e2e_steps}
+                      "d2h_bytes_per_step": dofs * 8, "steps": e2e_steps,
+                      "call": "per step: pdg_set_state (H2D) + pdg_step_lserk + pdg_get_state (D2H), i.e. the "
+                              "reference's step(disc, state, dt, stepper) with a host SolutionState"}
+        if ws == 1:
+            # informational: the production call, run_simulation (solver.cpp:591-666), K steps per call:
+            # state H2D once, energy (time, E) pair read back every step, state D2H once
+            k = args.steps
+            opts = pdg.capi.RunOptions(0.0, 0.5, dt, 0.0, 50, 10.0, 0, 0.0, pdg.capi.SNAPSHOT_CB(), None)
+            rr = pdg.capi.RunResult()
+            log = np.zeros(2 * (k + 2))
+            tt = C.c_double(0.0)
+            opts.final_time = k * dt
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            pdg.capi.check(lib.pdg_run_simulation(ctx.handle, hptr, C.byref(tt), C.byref(opts), C.byref(rr),
+                                                  log.ctypes.data_as(pdg.capi.DP), k + 2))
+            el = time.perf_counter() - t0
+            res["e2e_run_simulation"] = {
+                "value": dofs * rr.steps / el, "unit": UNIT, "steps": int(rr.steps),
+                "h2d_bytes_per_step": dofs * 8 / max(1, rr.steps),
+                "d2h_bytes_per_step": dofs * 8 / max(1, rr.steps) + 16,
+                "call": "pdg_run_simulation over the K timed steps: state in and out once, energy logged and read "
+                        "back every step, watchdog every 50 steps (informational; e2e above is the per-step call)"}
     ctx.close()
     del d, mesh
     return res
@@ -575,6 +597,7 @@ def main():
                        "parallelism": "single GPU",
                        "l2": "inputs larger than L2 (state >> 126 MB), no flush"},
             "roofline": head["roofline"], "cpu_baseline": cpu, "e2e": head.get("e2e"),
+            **({"e2e_run_simulation": head["e2e_run_simulation"]} if "e2e_run_simulation" in head else {}),
             "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
             "wedge_kernel_avg_ms": head["wedge_kernel_avg_ms"], "wedge_kernel_share": head["wedge_kernel_share"],
             **({k: head[k] for k in ("tet_kernel_avg_ms", "tet_kernel_share", "tet_roofline", "tensor_roofline")
