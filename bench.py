@@ -354,7 +354,8 @@ def measure_degree(args, degree, ws, rank, local, peaks, with_e2e=True):
             opts.final_time = k * dt
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            pdg.capi.check(lib.pdg_run_simulation(ctx.handle, hptr, C.byref(tt), C.byref(opts), C.byref(rr),
+            pdg.capi.check(lib.pdg_run_simulation(ctx.handle, C.cast(hptr, pdg.capi.DP), C.byref(tt), C.byref(opts),
+                                                  C.byref(rr),
                                                   log.ctypes.data_as(pdg.capi.DP), k + 2))
             el = time.perf_counter() - t0
             res["e2e_run_simulation"] = {

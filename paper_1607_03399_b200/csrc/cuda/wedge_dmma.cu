@@ -115,6 +115,9 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 // whole batch's streamed arrays into L2 (cp.async.bulk.prefetch.L2): the
 // elements after the next one get their HBM reads in flight early, without
 // shared memory or registers, so more bytes are in flight per SM
+#ifndef PDG_MEMONLY
+#define PDG_MEMONLY 0
+#endif
 #ifndef PDG_L2_PREFETCH
 #define PDG_L2_PREFETCH 0
 #endif
@@ -353,7 +356,11 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
   }
 
   const int mode = p.mode;
-  const bool vol = FUSED || (mode & M_VOLUME), surf = FUSED || (mode & M_SURFACE);
+  // PDG_MEMONLY (measurement only, never a product build): all arithmetic off,
+  // the same bulk copies, gathers-free, barriers and streaming stores -- the
+  // memory-side floor of this pipeline structure
+  const bool vol = !PDG_MEMONLY && (FUSED || (mode & M_VOLUME)),
+             surf = !PDG_MEMONLY && (FUSED || (mode & M_SURFACE));
   const bool lserk = FUSED || (mode & M_LSERK), media = FUSED || (mode & M_MEDIA);
   const bool first = mode & M_FIRST, accum = !FUSED && (mode & M_ACCUM);
   const double* res_src = lserk ? (first ? nullptr : p.res) : (accum ? p.rhs_out : nullptr);
@@ -606,7 +613,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
 #pragma unroll
         for (int jt = 0; jt < JTL; ++jt) {
           const double bp = src[jt][k];
-          dmma(lp[jt], la, bp);
+          if (!PDG_MEMONLY) dmma(lp[jt], la, bp);
           if (jt < JT) {
             const int jb = 8 * jt + gid;
             if (vol && !C::VF) {
@@ -615,7 +622,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
               dmma(dvx[jt], cx, Us[(NQ + jb) * SP + k]);
               dmma(dvy[jt], cy, Us[(2 * NQ + jb) * SP + k]);
             }
-            dmma(lv[jt], la, V[jb * VST + k]);
+            if (!PDG_MEMONLY) dmma(lv[jt], la, V[jb * VST + k]);
           }
         }
       }
