@@ -773,6 +773,17 @@ static void rhs_into(pdg_ctx* c, double* dst) {
   launch_checked(c, p, false);
 }
 
+// the AB3 step fused into the exact DMMA wedge stage kernel (wedge-only meshes,
+// N = 4..7); PDG_AB3_FUSED=0 keeps the rhs launch + update kernel
+static bool ab3_fused(const pdg_ctx* c) {
+  static const int env = [] {
+    const char* v = std::getenv("PDG_AB3_FUSED");
+    return v ? std::atoi(v) : 1;
+  }();
+  return env != 0 && c->Kt == 0 && !c->wadg && !c->wedge_simt && wedge_stage_ab3_supported(c->N) &&
+         !use_wedge_ws(c->N);
+}
+
 void step_ab3(pdg_ctx* c, double dt, int nsteps) {
   PDG_CK(cudaSetDevice(c->device));
   require_unpartitioned(c, "AB3");
@@ -790,8 +801,23 @@ void step_ab3(pdg_ctx* c, double dt, int nsteps) {
       ++c->ab3_filled;
       continue;
     }
-    rhs_into(c, c->fh[0]);
-    PDG_CK(launch_ab3_update((long long)nd, c->u[c->cur], c->fh[0], c->fh[1], c->fh[2], dt, c->stream));
+    if (ab3_fused(c)) {
+      // one launch: f_n into the free history slot and u_{n+1} into the other
+      // state buffer (the update kernel's arithmetic, in the stage epilogue)
+      StageParams p = base_params(c);
+      p.u_in = c->u[c->cur];
+      p.u_out = c->u[1 - c->cur];
+      p.rhs_out = c->fh[0];
+      p.h1 = c->fh[1];
+      p.h2 = c->fh[2];
+      p.dt = dt / 12.0;
+      p.mode = M_VOLUME | M_SURFACE | M_MEDIA | M_AB3;
+      launch_checked(c, p, true);
+      c->cur = 1 - c->cur;
+    } else {
+      rhs_into(c, c->fh[0]);
+      PDG_CK(launch_ab3_update((long long)nd, c->u[c->cur], c->fh[0], c->fh[1], c->fh[2], dt, c->stream));
+    }
     // h[2] <- h[1], h[1] <- f_n, the old h[2] becomes the free slot
     double* f2 = c->fh[2];
     c->fh[2] = c->fh[1];

@@ -98,6 +98,8 @@ enum : int {
   M_ACCUM = 8,     // rhs_out += (phase API) instead of =
   M_LSERK = 16,    // fused LSERK45 stage update instead of writing rhs
   M_FIRST = 32,    // a == 0: do not read res
+  M_AB3 = 64,      // fused AB3 step (exact DMMA wedge kernel): rhs_out = f_n, u_out = u_in + dt (23 f_n - 16 h1 + 5 h2)
+                   // with dt = the step / 12 (solver.cpp:575-577)
 };
 
 /// what a stage launcher did (host side, filled by every launcher): whether a
@@ -152,6 +154,8 @@ struct StageParams {
   unsigned long long* ticket_host_next; // host side: next base (advanced by the launcher)
   int ticket_batch;                     // consecutive elements per ticket (set by the launcher)
   LaunchInfo* info;                     // host side, may be null: filled by the launcher
+  const double* __restrict__ h1;        // M_AB3: f_{n-1}, f_{n-2}
+  const double* __restrict__ h2;
 };
 
 struct EnergyParams {
@@ -172,6 +176,7 @@ struct EnergyParams {
 
 // launchers (instantiated per degree in the .cu files)
 cudaError_t launch_wedge_stage(int N, const StageParams& p, cudaStream_t s); // FP64 tensor-core (DMMA) kernel
+bool wedge_stage_ab3_supported(int N); // the DMMA wedge kernel has the fused AB3 epilogue (M_AB3) at this N
 cudaError_t launch_tet_stage(int N, const StageParams& p, cudaStream_t s);
 /// warp-specialised wedge kernel (producer warp: tickets, TMA, gathers, fluxes; N = 4..7)
 bool wedge_ws_supported(int N);

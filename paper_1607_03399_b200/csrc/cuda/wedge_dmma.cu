@@ -127,7 +127,7 @@ __host__ __device__ constexpr int kmap(int s, int tig, int KS, bool perm) {
   return (perm && s < 4 * (KS / 4)) ? 16 * (s >> 2) + 4 * tig + (s & 3) : 4 * s + tig;
 }
 
-template <int N, int NST_>
+template <int N, int NST_, bool AB3_ = false>
 struct DCfg {
   // NP = device per-field block (NQ slices of ST doubles), ST = device slice stride
   static constexpr int NQ = nq_of(N), NT = nt_of(N), NP = npd_of(N), ST = nts_of(N), FW = fw_of(N), WG = wg_of(N);
@@ -140,7 +140,8 @@ struct DCfg {
   static constexpr int QF = PDG_COMPACT_OPS ? qcomp_of(N) : qfrag_of(N);
   // per-stage buffers (doubles), 16-byte aligned
   static constexpr int USTR = r4(4 * NP) + 2;
-  static constexpr int STAGE = r2(2 * USTR + LF + QF + WG + kWC / 2);
+  // AB3 mode: the residual slot holds f_{n-1}, a second slot after the records f_{n-2}
+  static constexpr int STAGE = r2(2 * USTR + LF + QF + WG + kWC / 2 + (AB3_ ? USTR : 0));
   // work buffers
   static constexpr bool KP = PDG_KPERM && (NT & 1) && ST == NT; // permuted k (odd slice stride)
   static constexpr int VST = KP ? NT : cf_stride(NT);        // V row stride (odd with KP)
@@ -201,17 +202,18 @@ __device__ __forceinline__ void team_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <int N, int NST>
+template <int N, int NST, bool AB3 = false>
 __device__ __forceinline__ void load_element(const StageParams& p, double* stg, long long e, const double* res_src,
                                              uint64_t* bar) {
-  using C = DCfg<N, NST>;
+  using C = DCfg<N, NST, AB3>;
   constexpr int NP = C::NP;
   double* U = stg;
   double* R = U + C::USTR;
   double* L = R + C::USTR;
   double* Q = L + C::LF;
   double* G = Q + C::QF;
-  const uint32_t bytes = 8u * (4 * NP + C::LF + C::QF + C::WG) + 4u * kWC + (res_src ? 32u * NP : 0u);
+  const uint32_t bytes = 8u * (4 * NP + C::LF + C::QF + C::WG) + 4u * kWC + (res_src ? 32u * NP : 0u) +
+                         (AB3 ? 32u * NP : 0u);
   // the state stays in L2 for the neighbours' trace gathers of this stage;
   // everything else is touched once
   const uint64_t keep = l2_policy_evict_last(), stream = l2_policy_evict_first();
@@ -222,6 +224,7 @@ __device__ __forceinline__ void load_element(const StageParams& p, double* stg, 
   tma_load_1d_hint(Q, p.QL + e * C::QF, 8 * C::QF, bar, stream);
   tma_load_1d_hint(G, p.wgeo + e * C::WG, 8 * C::WG, bar, stream);
   tma_load_1d_hint(G + C::WG, p.wconn + e * kWC, 4 * kWC, bar, stream);
+  if (AB3) tma_load_1d_hint(G + C::WG + kWC / 2, p.h2 + e * 4 * NP, 32 * NP, bar, stream);
 }
 
 /// warp `part` of T issues copies c = part, part + T, ... of the element's
@@ -260,9 +263,9 @@ __device__ __forceinline__ void load_element_part(const StageParams& p, double* 
   }
 }
 
-template <int N, bool COMBO_SMEM, bool FUSED, int NST>
-__global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(const StageParams p) {
-  using C = DCfg<N, NST>;
+template <int N, bool COMBO_SMEM, bool FUSED, int NST, bool AB3 = false>
+__global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kernel(const StageParams p) {
+  using C = DCfg<N, NST, AB3>;
   constexpr int NQ = C::NQ, NT = C::NT, NP = C::NP, ST = C::ST, FW = C::FW, WG = C::WG, T = C::T;
   constexpr int KS = C::KS, JT = C::JT, JTL = C::JTL, KT = C::KT, VST = C::VST, TPB = C::TPB;
   constexpr int QL_ = C::QF_LANE;
@@ -363,7 +366,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
              surf = !PDG_MEMONLY && (FUSED || (mode & M_SURFACE));
   const bool lserk = FUSED || (mode & M_LSERK), media = FUSED || (mode & M_MEDIA);
   const bool first = mode & M_FIRST, accum = !FUSED && (mode & M_ACCUM);
-  const double* res_src = lserk ? (first ? nullptr : p.res) : (accum ? p.rhs_out : nullptr);
+  const double* res_src = AB3 ? p.h1 : (lserk ? (first ? nullptr : p.res) : (accum ? p.rhs_out : nullptr));
   // dynamic scheduling keeps all teams on a narrow, L2-resident window of the
   // (Morton-ordered) element list, so neighbour traces hit in L2
   volatile long long* slot = reinterpret_cast<volatile long long*>(bar + 2);
@@ -390,7 +393,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
   if (grabber) {
     const long long e0 = grab();
     slot[0] = e0;
-    if (!SPLIT && e0 < p.Kw_active) load_element<N, NST>(p, stg0, e0, res_src, bar);
+    if (!SPLIT && e0 < p.Kw_active) load_element<N, NST, AB3>(p, stg0, e0, res_src, bar);
   }
   team_sync(bar_id, 32 * T);
   long long e = slot[0];
@@ -446,7 +449,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
     double* Fqu = Fqp + C::FQ;
     if (NST == 2 && !C::NOEND && tt == 0 && en < p.Kw_active) {
       fence_proxy_async_smem();
-      load_element<N, NST>(p, stg0 + (s ^ 1) * C::STAGE, en, res_src, bar + (s ^ 1));
+      load_element<N, NST, AB3>(p, stg0 + (s ^ 1) * C::STAGE, en, res_src, bar + (s ^ 1));
     }
     mbar_wait(bar + s, NST == 2 ? ((n >> 1) & 1) : (n & 1));
 
@@ -539,7 +542,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
     // every warp of the team has left the previous element: its stage may be refilled
     if (C::NOEND && !SPLIT && tt == 0 && en < p.Kw_active) {
       fence_proxy_async_smem();
-      load_element<N, NST>(p, stg0 + (s ^ 1) * C::STAGE, en, res_src, bar + (s ^ 1));
+      load_element<N, NST, AB3>(p, stg0 + (s ^ 1) * C::STAGE, en, res_src, bar + (s ^ 1));
     }
     if (SPLIT && lane == 0) {
       const long long enx = slot[1 + (n & 1)]; // written before the flux barrier by the grabber
@@ -685,6 +688,7 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
       const int lane_off = 2 * tig * ST + i;
       const double* Ul = Us + 2 * tig * SP + i; // padded rows: (field*NQ + j)*SP + i
       const double* Rl = R + lane_off;
+      const double* F2l = G + WG + kWC / 2 + lane_off; // AB3: f_{n-2} (stage slot after the records)
       const long long gofs = e * 4 * NP + lane_off;
       double* resl = p.res + gofs;
       double* uol = p.u_out + gofs;
@@ -723,7 +727,12 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
             for (int f = 0; f < 4; ++f) {
               const int o = f * NP + 8 * jt * ST + cst[c];
               const int ou = (f * NQ + 8 * jt) * SP + csp[c];
-              if (lserk) {
+              if (AB3) {
+                // f_n to the history slot; u_{n+1} = u_n + dt/12 (23 f_n - 16 f_{n-1} + 5 f_{n-2})
+                // with pdt = dt/12 and the update kernel's operation order (bitwise equal)
+                __stcs(rhsl + o, rv[f]);
+                __stcs(uol + o, Ul[ou] + pdt * (23.0 * rv[f] - 16.0 * Rl[o] + 5.0 * F2l[o]));
+              } else if (lserk) {
                 const double rr = first ? pdt * rv[f] : pa * Rl[o] + pdt * rv[f];
                 __stcs(resl + o, rr); // streaming stores: evict first
                 __stcs(uol + o, Ul[ou] + pb * rr);
@@ -735,20 +744,20 @@ __global__ void __launch_bounds__(DCfg<N, NST>::THREADS, 1) wedge_dmma_kernel(co
         }
     }
     if (!C::NOEND) team_sync(bar_id, 32 * T); // stage s and the work buffers are free again
-    if (NST == 1 && tt == 0 && en < p.Kw_active) load_element<N, NST>(p, stg0, en, res_src, bar);
+    if (NST == 1 && tt == 0 && en < p.Kw_active) load_element<N, NST, AB3>(p, stg0, en, res_src, bar);
     e = slot[1 + (n & 1)];
   }
 }
 
-template <int N, bool CS, bool FUSED, int NST>
+template <int N, bool CS, bool FUSED, int NST, bool AB3 = false>
 cudaError_t launch_dmma_NC(const StageParams& p, cudaStream_t s) {
-  using C = DCfg<N, NST>;
+  using C = DCfg<N, NST, AB3>;
   // one-time setup per device (the smem attribute is per device)
   static int grid_cap[kMaxDevices] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= kMaxDevices) return cudaErrorInvalidDevice;
-  auto kern = wedge_dmma_kernel<N, CS, FUSED, C::NSTAGE>;
+  auto kern = wedge_dmma_kernel<N, CS, FUSED, C::NSTAGE, AB3>;
   if (grid_cap[dev] == 0) {
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM_BYTES);
     if (err != cudaSuccess) return err;
@@ -781,6 +790,11 @@ cudaError_t launch_dmma_N(const StageParams& p, cudaStream_t s) {
     const char* v = std::getenv("PDG_WEDGE_STAGES");
     return (v && v[0] == '1') ? 1 : kWedgeStages;
   }();
+  if (p.mode & M_AB3) {
+    if constexpr (N >= 4 && N <= 7)
+      return cs ? launch_dmma_NC<N, true, false, 2, true>(p, s) : launch_dmma_NC<N, false, false, 2, true>(p, s);
+    return cudaErrorInvalidValue;
+  }
   if (stages == 1) {
     if (fused) return cs ? launch_dmma_NC<N, true, true, 1>(p, s) : launch_dmma_NC<N, false, true, 1>(p, s);
     return cs ? launch_dmma_NC<N, true, false, 1>(p, s) : launch_dmma_NC<N, false, false, 1>(p, s);
@@ -802,6 +816,8 @@ cudaError_t launch_wedge_stage(int N, const StageParams& p, cudaStream_t s) {
 }
 
 bool wedge_dmma_compact_ops() { return PDG_COMPACT_OPS != 0; }
+
+bool wedge_stage_ab3_supported(int N) { return N >= 4 && N <= 7; }
 
 int wedge_elems_per_block(int N) {
   switch (N) {
