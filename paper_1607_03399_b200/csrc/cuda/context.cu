@@ -145,6 +145,19 @@ bool use_wedge_ws(int N) {
   return wedge_ws_supported(N) && env != 0 && (env > 0 || PDG_WEDGE_WS_DEFAULT);
 }
 
+// exact-mode wedge kernel for N <= 3: the thread-per-DOF-column kernel
+// (wedge_lo.cu) when PDG_WEDGE_LO=1 (or PDG_WEDGE_LO_DEFAULT), else wedge_simt.cu
+#ifndef PDG_WEDGE_LO_DEFAULT
+#define PDG_WEDGE_LO_DEFAULT 0
+#endif
+bool use_wedge_lo(int N) {
+  static const int env = [] {
+    const char* v = std::getenv("PDG_WEDGE_LO");
+    return v ? std::atoi(v) : -1;
+  }();
+  return wedge_lo_supported(N) && env != 0 && (env > 0 || PDG_WEDGE_LO_DEFAULT);
+}
+
 void launch_checked(pdg_ctx* c, const StageParams& p0, bool wedge) {
   cudaEvent_t a = nullptr, b = nullptr;
   if (c->flags & 2) {
@@ -158,7 +171,8 @@ void launch_checked(pdg_ctx* c, const StageParams& p0, bool wedge) {
   cudaError_t err = !wedge ? launch_tet_stage(c->N, p, c->stream)
                     : c->wadg ? (c->N <= wedge_wadg_simt_max_degree() ? launch_wedge_wadg_simt_stage(c->N, p, c->stream)
                                                                      : launch_wedge_wadg_stage(c->N, p, c->stream))
-                    : c->wedge_simt ? launch_wedge_simt_stage(c->N, p, c->stream)
+                    : c->wedge_simt ? (use_wedge_lo(c->N) ? launch_wedge_lo_stage(c->N, p, c->stream)
+                                                          : launch_wedge_simt_stage(c->N, p, c->stream))
                     : use_wedge_ws(c->N) ? launch_wedge_ws_stage(c->N, p, c->stream)
                                          : launch_wedge_stage(c->N, p, c->stream);
   if (err != cudaSuccess) {
