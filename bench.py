@@ -388,7 +388,9 @@ def measure_degree_dist(args, degree, ws, rank, local, peaks):
         part = P.layered_strong(args.strong_n, [-1.0, -0.4, 0.2, 1.0], args.sublayers, media, ws, rank)
     else:
         part = P.layered_slab(args.surface_n, [-1.0, -0.4, 0.2, 1.0], args.sublayers, media, ws, rank)
-    solver = DistributedLSERK(part, degree, device=local, threads=os.cpu_count() or 1, flags=pdg.capi.CTX_TIMING)
+    # host setup threads split between the ranks of this node (no oversubscription)
+    threads = max(1, (os.cpu_count() or 1) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", ws))))
+    solver = DistributedLSERK(part, degree, device=local, threads=threads, flags=pdg.capi.CTX_TIMING)
     d = solver.disc
     s = pdg.make_initial_state(d, "gaussian", [0.25, 0.0, 0.0, 0.0])
     dt = pdg.estimate_dt(d, 0.5)
@@ -478,7 +480,11 @@ def relaunch(args):
     sk.close()
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
-    return subprocess.call(cmd)
+    # torchrun would pin every rank to one OpenMP thread; the host setup of a
+    # 1e6-wedge partition wants the node's cores split between the ranks
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", str(max(1, (os.cpu_count() or 1) // args.gpus)))
+    return subprocess.call(cmd, env=env)
 
 
 def main():
