@@ -62,6 +62,24 @@ constexpr int kComboCapT = 2048; // ints of neighbour node maps kept in shared m
 #endif
 __host__ __device__ constexpr bool tet_tables_global(int N) { return N >= PDG_TET_TG_MIN_N; }
 
+// residual loads issued after the flux phase instead of at the start of the batch
+// (frees 16 registers across the gathers), and the face-node task indices
+// recomputed in the flux loop instead of kept live across the gathers (at N = 4
+// they were spilled to local memory, the hottest stall of the kernel).  Measured
+// together (profiles/round2_tet_ab.txt): N = 3 / 4 / 5 -3.4 / -3.8 / -2.3%
+#ifndef PDG_TET_RES_LATE
+#define PDG_TET_RES_LATE 1
+#endif
+#ifndef PDG_TET_LAUNDER
+#define PDG_TET_LAUNDER 1
+#endif
+// DMMA issue order of the volume products: 0 = gr gs gt dv dv dv, 1 = gr dv gs dv gt dv
+// (measured equal: DMMA latency is 26 cycles against a 16-cycle issue interval per
+// SM sub-partition, scripts/micro/dmma_latency.cu, so two chains already saturate)
+#ifndef PDG_TET_ORDER
+#define PDG_TET_ORDER 0
+#endif
+
 #ifndef PDG_TET_PAD_STATE
 #define PDG_TET_PAD_STATE 1
 #endif
@@ -244,6 +262,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
     // residual (or accumulated rhs) of this thread's 2 tets x 4 fields, loaded
     // now so the HBM latency overlaps the flux and product phases
     double rres[2][4];
+    auto load_res = [&]() {
 #pragma unroll
     for (int c = 0; c < 2; ++c)
 #pragma unroll
@@ -252,6 +271,8 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
         rres[c][fld] = (res_src && n < NP && t < nel)
                            ? __ldcs(res_src + p.tet_base + (t0 + t) * 4 * NP + fld * NP + n) : 0.0;
       }
+    };
+    if (!PDG_TET_RES_LATE) load_res();
 
     // the W_a columns of the volume products (P, r/s/t-combinations of the velocity)
     // measured (profiles/round1_tet_bv_ab.txt): N = 3 -0.9%, N = 5 -0.6%, N = 6 -1.7%, N = 4 +2.5% (spills)
@@ -304,7 +325,8 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
       if (kBvFirst) build_bv(); // shared-memory work while the gathers are in flight
 #pragma unroll
       for (int q = 0; q < C::TASKS; ++q) {
-        const int m = tt + 32 * T * q;
+        int m = tt + 32 * T * q;
+        if (PDG_TET_LAUNDER) asm volatile("" : "+r"(m)); // recomputed, not kept live
         if (m < nel * 4 * NT) {
           const int t = m / (4 * NT), fm = m - t * 4 * NT;
           const int f = fm / NT, loc = fm - f * NT;
@@ -333,6 +355,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
       }
     }
     if (!kBvFirst) build_bv();
+    if (PDG_TET_RES_LATE) load_res();
     team_sync(bar_id, 32 * T);
 
     // ---- row tile w: volume and lift products -------------------------------------
@@ -345,12 +368,21 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
         const double ar = tab(sD, fo), as = tab(sD, C::DTAB + fo), at = tab(sD, 2 * C::DTAB + fo);
         const int bo = gid * VST + 4 * s2 + tig;
         const double bp = BVb[bo];
-        dmma(gr, ar, bp);
-        dmma(gs, as, bp);
-        dmma(gt, at, bp);
-        dmma(dv, ar, BVb[kTB * VST + bo]);
-        dmma(dv, as, BVb[2 * kTB * VST + bo]);
-        dmma(dv, at, BVb[3 * kTB * VST + bo]);
+        if (PDG_TET_ORDER == 1) {
+          dmma(gr, ar, bp);
+          dmma(dv, ar, BVb[kTB * VST + bo]);
+          dmma(gs, as, bp);
+          dmma(dv, as, BVb[2 * kTB * VST + bo]);
+          dmma(gt, at, bp);
+          dmma(dv, at, BVb[3 * kTB * VST + bo]);
+        } else {
+          dmma(gr, ar, bp);
+          dmma(gs, as, bp);
+          dmma(gt, at, bp);
+          dmma(dv, ar, BVb[kTB * VST + bo]);
+          dmma(dv, as, BVb[2 * kTB * VST + bo]);
+          dmma(dv, at, BVb[3 * kTB * VST + bo]);
+        }
       }
     }
     if (surf) {
