@@ -80,6 +80,13 @@ __host__ __device__ constexpr bool tet_tables_global(int N) { return N >= PDG_TE
 #define PDG_TET_ORDER 0
 #endif
 
+// the next batch index in two slots alternating with the batch parity: a slot is
+// rewritten only after every thread has read it, so the barrier that protected
+// the single slot goes (two team barriers per batch instead of three)
+#ifndef PDG_TET_SLOT_PARITY
+#define PDG_TET_SLOT_PARITY 0
+#endif
+
 #ifndef PDG_TET_PAD_STATE
 #define PDG_TET_PAD_STATE 1
 #endif
@@ -114,8 +121,9 @@ struct TDCfg {
   static constexpr int BF = 4 * kTB * FST;    // [face][tet][face node]
   static constexpr int WORK = BV + 2 * BF;
   static constexpr int SMEM_BUDGET = 225 * 1024;
-  static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 4 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
-  static constexpr int PER_TEAM = 4 + NSTAGE * STAGE + WORK;
+  static constexpr int HDR = PDG_TET_SLOT_PARITY ? 6 : 4; // 2 mbarriers + 2 (3) slots
+  static constexpr int NSTAGE = (NST_ == 2 && (TABLES + HDR + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
+  static constexpr int PER_TEAM = HDR + NSTAGE * STAGE + WORK;
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
   static constexpr int TPB = cmax(1, cmin(cmin(8, cmax(1, PDG_TET_CAP(N) / (32 * T))), TPB_SMEM));
   static constexpr int THREADS = 32 * T * TPB;
@@ -209,7 +217,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
   const int bar_id = 1 + team;
   double* tbase = smem + C::TABLES + (size_t)team * C::PER_TEAM;
   uint64_t* bar = reinterpret_cast<uint64_t*>(tbase);
-  double* stg0 = tbase + 4;
+  double* stg0 = tbase + C::HDR;
   double* BVb = stg0 + NST * C::STAGE; // column (g * 8 + tet) at g*8+tet times VST
   double* FPb = BVb + C::BV;           // column (face * 8 + tet) times FST
   double* FUb = FPb + C::BF;
@@ -246,7 +254,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
     long long bn = 0;
     if (tt == 0) {
       bn = grab();
-      slot[1] = bn;
+      slot[PDG_TET_SLOT_PARITY ? 1 + (it & 1) : 1] = bn;
     }
     const double* U = stg0 + s * C::STAGE;
     const double* G = U + C::UB;
@@ -444,8 +452,8 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
     }
     team_sync(bar_id, 32 * T); // stage s and the work buffers are free again
     if (NST == 1 && tt == 0 && bn < nbatch) load_batch<N, NST>(p, stg0, p.Kt_begin + bn * kTB, nel_of(bn), bar);
-    b = slot[1];
-    team_sync(bar_id, 32 * T);
+    b = slot[PDG_TET_SLOT_PARITY ? 1 + (it & 1) : 1];
+    if (!PDG_TET_SLOT_PARITY) team_sync(bar_id, 32 * T);
   }
 }
 

@@ -122,6 +122,24 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #define PDG_L2_PREFETCH 0
 #endif
 
+// the two per-element team exchanges (fluxes -> products, V -> its lift) through
+// mbarriers instead of bar.sync: a warp arrives when its part is written and waits
+// only where it reads the others' part, so V-independent products (the lifts of
+// [P | Fu0 | Fu1], LY and the quad-face lifts) run between the V arrival and the
+// V wait, and (PDG_MB_VOL_AFTER, where the volume products are not issued first)
+// the element's volume products between the flux arrival and the flux wait.
+// Measured (profiles/round2_mbar_ab.txt): N = 5 -1.7% (adopted), N = 4 +0.4%;
+// volume products after the flux arrival +1.3% at N = 5 (not adopted)
+#ifndef PDG_MBAR_SYNC_N6
+#define PDG_MBAR_SYNC_N6 0
+#endif
+#ifndef PDG_MBAR_SYNC
+#define PDG_MBAR_SYNC(N) ((N) == 5 || ((N) == 6 && PDG_MBAR_SYNC_N6))
+#endif
+#ifndef PDG_MB_VOL_AFTER
+#define PDG_MB_VOL_AFTER 0
+#endif
+
 /// k index of lane column tig in k-step s (see PDG_KPERM)
 __host__ __device__ constexpr int kmap(int s, int tig, int KS, bool perm) {
   return (perm && s < 4 * (KS / 4)) ? 16 * (s >> 2) + 4 * tig + (s & 3) : 4 * s + tig;
@@ -163,12 +181,18 @@ struct DCfg {
   static constexpr int TABLES = r2(2 * IT * KS * 32 + JT * KT * 32 + 2 * NQ + ceil_div(FW, 2) + kComboCap / 2);
   static constexpr int SMEM_BUDGET = 225 * 1024;
   // double-buffered stages unless even a single team would not fit
-  static constexpr int NSTAGE = (NST_ == 2 && (TABLES + 6 + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
-  static constexpr int PER_TEAM = 6 + NSTAGE * STAGE + WORK;
+  // team header: 2 stage mbarriers + 3 schedule slots (+ 2 exchange mbarriers)
+  static constexpr int HDR = PDG_MBAR_SYNC(N) ? 8 : 6;
+  static constexpr int NSTAGE = (NST_ == 2 && (TABLES + HDR + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
+  static constexpr int PER_TEAM = HDR + NSTAGE * STAGE + WORK;
   static constexpr bool NOEND = FBUF == 2 && NSTAGE == 2;
+  // mbarrier exchanges need the parity flux buffers (no end-of-element barrier)
+  static constexpr bool MB = PDG_MBAR_SYNC(N) && NOEND && !PDG_SPLIT_ISSUE;
   // measured (profiles/round1_volfirst_ab.txt): N = 4 -2.8%, N = 6 -4.5%, N = 7 -6.5%,
   // N = 5 +0.4% (with the dropped end barrier its gathers are already covered)
   static constexpr bool VF = PDG_VOL_FIRST && (N != 5 || PDG_VF_N5);
+  static constexpr bool VA = MB && !VF && PDG_MB_VOL_AFTER; // volume products after the flux arrival
+  static constexpr bool VP = VF || VA;                      // volume products outside G1 / G2
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
   // <= PDG_THREAD_CAP threads per CTA: 384 keeps >= 168 registers per thread
   // (profiles/round1_compact_ops_ab.txt: compact operators + 384 beat 512)
@@ -305,7 +329,9 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
   const int bar_id = 1 + team;
   double* tbase = smem + C::TABLES + (size_t)team * C::PER_TEAM;
   uint64_t* bar = reinterpret_cast<uint64_t*>(tbase);
-  double* stg0 = tbase + 6; // 2 mbarriers + 3 schedule slots + pad
+  double* stg0 = tbase + C::HDR; // 2 mbarriers + 3 schedule slots (+ 2 exchange mbarriers) + pad
+  uint64_t* fbar = bar + 5;      // C::MB: flux exchange
+  uint64_t* vbar = bar + 6;      // C::MB: V exchange
   double* V = stg0 + NST * C::STAGE;
   double* const Fbase = V + C::VS; // C::FBUF sets of flux buffers (element parity)
   const double* Zero = Fbase + C::FBUF * C::FB; // ZS zeros, never written
@@ -316,6 +342,10 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
   if (tt == 0) {
     mbar_init(bar, SPLIT ? T : 1);
     mbar_init(bar + 1, SPLIT ? T : 1);
+    if (C::MB) {
+      mbar_init(fbar, 32 * T);
+      mbar_init(vbar, 32 * T);
+    }
     fence_barrier_init();
   }
   __syncthreads();
@@ -467,8 +497,7 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
     for (int jt = 0; jt < JT; ++jt)
 #pragma unroll
       for (int c = 0; c < 2; ++c) gx[jt][c] = gy[jt][c] = dvx[jt][c] = dvy[jt][c] = dg1[jt][c] = 0.0;
-    if (C::VF) {
-      if (surf) gather(Cn);
+    auto volume_products = [&]() {
       if (vol) {
         const int i = 8 * w + gid;
         const double tzJ = G[W_TZJ];
@@ -503,6 +532,10 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
           }
         }
       }
+    };
+    if (C::VF) {
+      if (surf) gather(Cn);
+      volume_products();
     }
 
     // ---- numerical fluxes on all face nodes -------------------------------------
@@ -538,7 +571,13 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
         }
       }
     }
-    team_sync(bar_id, 32 * T);
+    if (C::MB) {
+      mbar_arrive(fbar);
+      if (C::VA) volume_products(); // own state only: covers the other warps' fluxes
+      mbar_wait(fbar, n & 1);
+    } else {
+      team_sync(bar_id, 32 * T);
+    }
     // every warp of the team has left the previous element: its stage may be refilled
     if (C::NOEND && !SPLIT && tt == 0 && en < p.Kw_active) {
       fence_proxy_async_smem();
@@ -560,7 +599,7 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
 #pragma unroll
       for (int jt = 0; jt < JT; ++jt) {
         double d[2] = {dg1[jt][0], dg1[jt][1]};
-        if (vol && !C::VF) {
+        if (vol && !C::VP) {
           const int jb = 8 * jt + gid;
           const int jc = jb < NQ ? jb : NQ - 1;
           const double sx_ = G[W_TXJ + jc], sy_ = G[w_tyj(N) + jc];
@@ -580,7 +619,10 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
         }
       }
     }
-    team_sync(bar_id, 32 * T);
+    if (C::MB)
+      mbar_arrive(vbar); // L V waits for it after the V-independent products
+    else
+      team_sync(bar_id, 32 * T);
 
     // ---- row tile w: G2, G3, G4, G5 and the epilogue ---------------------------
     {
@@ -608,7 +650,7 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
         const double la = Lf[fo];
 #endif
         double cx = 0.0, cy = 0.0;
-        if (vol && !C::VF) {
+        if (vol && !C::VP) {
           const double dr = dr_of(s2), ds = ds_of(s2);
           cx = rx * dr + sxm * ds;
           cy = ry * dr + sym * ds;
@@ -619,13 +661,13 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
           if (!PDG_MEMONLY) dmma(lp[jt], la, bp);
           if (jt < JT) {
             const int jb = 8 * jt + gid;
-            if (vol && !C::VF) {
+            if (vol && !C::VP) {
               dmma(gx[jt], cx, bp);
               dmma(gy[jt], cy, bp);
               dmma(dvx[jt], cx, Us[(NQ + jb) * SP + k]);
               dmma(dvy[jt], cy, Us[(2 * NQ + jb) * SP + k]);
             }
-            if (!PDG_MEMONLY) dmma(lv[jt], la, V[jb * VST + k]);
+            if (!PDG_MEMONLY && !C::MB) dmma(lv[jt], la, V[jb * VST + k]);
           }
         }
       }
@@ -674,6 +716,21 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
               dmma(qu[f][jt], qa, Fqu[fo]);
             }
           }
+      }
+      if (C::MB && !PDG_MEMONLY) {
+        // L V once every warp's V rows are in
+        mbar_wait(vbar, n & 1);
+#pragma unroll
+        for (int s2 = 0; s2 < KS; ++s2) {
+          const int k = kmap(s2, tig, KS, C::KP);
+#if PDG_COMPACT_OPS
+          const double la = (i < NT && k < NT) ? Lf[k * NT + i] : 0.0;
+#else
+          const double la = Lf[((t * KS + s2) << 5) + lane];
+#endif
+#pragma unroll
+          for (int jt = 0; jt < JT; ++jt) dmma(lv[jt], la, V[(8 * jt + gid) * VST + k]);
+        }
       }
       // epilogue: rows i, columns j = 8 jt + 2 tig + c; results straight to HBM
       const double tzJ = G[W_TZJ], jfb = G[W_JFB], jft = G[W_JFT];

@@ -63,6 +63,12 @@ constexpr int kComboCapW = 2048; // ints of neighbour node maps kept in shared m
 #ifndef PDG_WADG_VOL_FIRST
 #define PDG_WADG_VOL_FIRST 1
 #endif
+// the pre-lift buffer exchange through an mbarrier instead of bar.sync: a warp
+// arrives when its rows of B are written, forms its Ltilde rows (phase A, which
+// needs only 1/J at the cubature) and then waits for the other warps' rows
+#ifndef PDG_WADG_MB
+#define PDG_WADG_MB 0
+#endif
 #ifndef PDG_WADG_NOEND_MAX_N
 #define PDG_WADG_NOEND_MAX_N 7
 #endif
@@ -256,9 +262,12 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
   double* const Fbase = Bb + C::BS;   // C::FBUF sets of {Ftp, Ftu, Fqp, Fqu, 1/J} (element parity)
   double* Upad = Fbase + C::FBUF * C::FBW; // padded state copy (C::PAD)
   constexpr int SP = C::SP;
+  constexpr bool MB = PDG_WADG_MB && C::NOEND;
+  uint64_t* vbar = bar + 5; // MB: pre-lift buffer exchange
   if (tt == 0) {
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
+    if (MB) mbar_init(vbar, 32 * T);
     fence_barrier_init();
   }
   __syncthreads();
@@ -469,6 +478,7 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
     const int i = 8 * t + gid;
     // ---- A: Ltilde rows of tile t (columns = tri nodes, IT column tiles) ------
     double lt[IT][2];
+    auto ltilde = [&]() {
 #pragma unroll
     for (int ct = 0; ct < IT; ++ct) lt[ct][0] = lt[ct][1] = 0.0;
 #pragma unroll
@@ -477,6 +487,8 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
 #pragma unroll
       for (int ct = 0; ct < IT; ++ct) dmma(lt[ct], a, tab(tVq, ((ct * KQ + s2) << 5) + lane));
     }
+    };
+    if (!MB) ltilde();
 
     if (!C::VF) vol_products();
 
@@ -549,7 +561,13 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
           }
         }
     }
-    team_sync(bar_id, 32 * T);
+    if (MB) {
+      mbar_arrive(vbar);
+      ltilde(); // needs only 1/J: covers the other warps' pre-lift rows
+      mbar_wait(vbar, n & 1);
+    } else {
+      team_sync(bar_id, 32 * T);
+    }
 
     // ---- F: rhs rows of tile t = Ltilde B ------------------------------------------
     double acc[CT][2];
