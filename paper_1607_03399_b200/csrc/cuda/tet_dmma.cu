@@ -87,6 +87,14 @@ __host__ __device__ constexpr bool tet_tables_global(int N) { return N >= PDG_TE
 #define PDG_TET_SLOT_PARITY 0
 #endif
 
+// end-of-batch barrier through an mbarrier (needs the slot parity and two stages):
+// a warp arrives when it has finished the batch and only waits for the others
+// right before it writes the work buffers of the next batch (after issuing that
+// batch's neighbour gathers); thread 0 refills the freed stage after that wait
+#ifndef PDG_TET_END_MBAR
+#define PDG_TET_END_MBAR 0
+#endif
+
 #ifndef PDG_TET_PAD_STATE
 #define PDG_TET_PAD_STATE 1
 #endif
@@ -221,9 +229,12 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
   double* BVb = stg0 + NST * C::STAGE; // column (g * 8 + tet) at g*8+tet times VST
   double* FPb = BVb + C::BV;           // column (face * 8 + tet) times FST
   double* FUb = FPb + C::BF;
+  constexpr bool TMB = PDG_TET_END_MBAR && PDG_TET_SLOT_PARITY && NST == 2;
+  uint64_t* ebar = bar + 5; // TMB: end of batch
   if (tt == 0) {
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
+    if (TMB) mbar_init(ebar, 32 * T);
     fence_barrier_init();
   }
   __syncthreads();
@@ -259,10 +270,22 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
     const double* U = stg0 + s * C::STAGE;
     const double* G = U + C::UB;
     const int* Cn = reinterpret_cast<const int*>(G + kTB * kTG);
-    if (NST == 2 && tt == 0 && bn < nbatch) {
+    if (NST == 2 && !TMB && tt == 0 && bn < nbatch) {
       fence_proxy_async_smem();
       load_batch<N, NST>(p, stg0 + (s ^ 1) * C::STAGE, p.Kt_begin + bn * kTB, nel_of(bn), bar + (s ^ 1));
     }
+    // TMB: every thread has finished the previous batch (its stage and the work
+    // buffers are free) -- waited once, before the first work-buffer write
+    bool waited = !TMB;
+    auto end_wait = [&]() {
+      if (waited) return;
+      waited = true;
+      if (it > 0) mbar_wait(ebar, (it - 1) & 1);
+      if (tt == 0 && bn < nbatch) {
+        fence_proxy_async_smem();
+        load_batch<N, NST>(p, stg0 + (s ^ 1) * C::STAGE, p.Kt_begin + bn * kTB, nel_of(bn), bar + (s ^ 1));
+      }
+    };
     mbar_wait(bar + s, NST == 2 ? ((it >> 1) & 1) : (it & 1));
     const long long t0 = p.Kt_begin + b * kTB;
     const int nel = nel_of(b);
@@ -300,7 +323,10 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
     }
     };
     // ---- fluxes of the batch (scaled by J_f / J) and the W_a columns ------------
-    if (kBvFirst && !surf) build_bv();
+    if (kBvFirst && !surf) {
+      end_wait();
+      build_bv();
+    }
     if (surf) {
       // all gathers of this thread's face-node tasks first (independent loads in
       // flight together), then the flux arithmetic
@@ -330,6 +356,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
           }
         }
       }
+      end_wait();
       if (kBvFirst) build_bv(); // shared-memory work while the gathers are in flight
 #pragma unroll
       for (int q = 0; q < C::TASKS; ++q) {
@@ -362,6 +389,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
         }
       }
     }
+    end_wait();
     if (!kBvFirst) build_bv();
     if (PDG_TET_RES_LATE) load_res();
     team_sync(bar_id, 32 * T);
@@ -450,7 +478,10 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
         }
       }
     }
-    team_sync(bar_id, 32 * T); // stage s and the work buffers are free again
+    if (TMB)
+      mbar_arrive(ebar);
+    else
+      team_sync(bar_id, 32 * T); // stage s and the work buffers are free again
     if (NST == 1 && tt == 0 && bn < nbatch) load_batch<N, NST>(p, stg0, p.Kt_begin + bn * kTB, nel_of(bn), bar);
     b = slot[PDG_TET_SLOT_PARITY ? 1 + (it & 1) : 1];
     if (!PDG_TET_SLOT_PARITY) team_sync(bar_id, 32 * T);

@@ -140,6 +140,14 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #define PDG_MB_VOL_AFTER 0
 #endif
 
+// at N = 6, 7 the last 8-column tile of the [P | Fu0 | Fu1] product holds only the
+// tri-face velocity fluxes (1 or 2 of 8 columns): those lifts are dot products on
+// the FP64 cores instead (the lane's A fragment times the flux at its k, reduced
+// over the lane quad), one DMMA per k-step less
+#ifndef PDG_FU_DOT
+#define PDG_FU_DOT 0
+#endif
+
 /// k index of lane column tig in k-step s (see PDG_KPERM)
 __host__ __device__ constexpr int kmap(int s, int tig, int KS, bool perm) {
   return (perm && s < 4 * (KS / 4)) ? 16 * (s >> 2) + 4 * tig + (s & 3) : 4 * s + tig;
@@ -152,6 +160,9 @@ struct DCfg {
   static constexpr int IT = it_of(N), KS = ks_of(N), KT = kt_of(N);
   static constexpr int JT = ceil_div(NQ, 8), NPJ = 8 * JT;   // slice column tiles
   static constexpr int JTL = ceil_div(NQ + 2, 8);            // [P | Fu0 | Fu1] tiles
+  static constexpr bool FUV = PDG_FU_DOT && 8 * (JTL - 1) >= NQ; // last tile = fluxes only
+  static constexpr int JL = FUV ? JTL - 1 : JTL;               // tiles on the tensor cores
+  static constexpr bool DOT0 = FUV && NQ >= 8 * (JTL - 1);     // Fu0 in the last tile too
   static constexpr int T = IT;                               // warps per team
   // per-wedge operator block sizes in HBM / the stage buffer
   static constexpr int LF = PDG_COMPACT_OPS ? lcomp_of(N) : lfrag_of(N);
@@ -635,7 +646,8 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
         const int nc = 8 * jt + gid;
         src[jt] = nc < NQ ? Us + nc * SP : (nc == NQ ? Ftu : (nc == NQ + 1 ? Ftu + NT : Zero));
       }
-      double lv[JT][2], lp[JTL][2];
+      constexpr int JL = C::JL;
+      double lv[JT][2], lp[JTL][2], d0 = 0.0, d1 = 0.0; // d0, d1: C::FUV dot products
 #pragma unroll
       for (int jt = 0; jt < JT; ++jt) lv[jt][0] = lv[jt][1] = 0.0;
 #pragma unroll
@@ -655,10 +667,14 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
           cx = rx * dr + sxm * ds;
           cy = ry * dr + sym * ds;
         }
+        if (C::FUV && !PDG_MEMONLY) {
+          if (C::DOT0) d0 = fma(la, Ftu[k], d0);
+          d1 = fma(la, Ftu[NT + k], d1);
+        }
 #pragma unroll
         for (int jt = 0; jt < JTL; ++jt) {
-          const double bp = src[jt][k];
-          if (!PDG_MEMONLY) dmma(lp[jt], la, bp);
+          const double bp = jt < JL ? src[jt][k] : 0.0;
+          if (!PDG_MEMONLY && jt < JL) dmma(lp[jt], la, bp);
           if (jt < JT) {
             const int jb = 8 * jt + gid;
             if (vol && !C::VP) {
@@ -688,8 +704,14 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
       }
       // L fu_bottom, L fu_top of this row (columns NQ, NQ+1 of the G3 product)
       constexpr int c0 = NQ % 8, c1 = (NQ + 1) % 8;
-      const double lf0 = __shfl_sync(0xffffffffu, lp[NQ / 8][c0 & 1], gid * 4 + c0 / 2);
-      const double lf1 = __shfl_sync(0xffffffffu, lp[(NQ + 1) / 8][c1 & 1], gid * 4 + c1 / 2);
+      if (C::FUV) { // sum the lane quad's partial dot products
+        if (C::DOT0) d0 += __shfl_xor_sync(0xffffffffu, d0, 1);
+        d1 += __shfl_xor_sync(0xffffffffu, d1, 1);
+        if (C::DOT0) d0 += __shfl_xor_sync(0xffffffffu, d0, 2);
+        d1 += __shfl_xor_sync(0xffffffffu, d1, 2);
+      }
+      const double lf0 = C::DOT0 ? d0 : __shfl_sync(0xffffffffu, lp[NQ / 8][c0 & 1], gid * 4 + c0 / 2);
+      const double lf1 = C::FUV ? d1 : __shfl_sync(0xffffffffu, lp[(NQ + 1) / 8][c1 & 1], gid * 4 + c1 / 2);
       // G5: quad-face lifts; the velocity lift of each face is kept separately
       // and scaled by that face's normal in the epilogue
       double qp[JT][2], qu[3][JT][2];

@@ -65,9 +65,11 @@ constexpr int kComboCapW = 2048; // ints of neighbour node maps kept in shared m
 #endif
 // the pre-lift buffer exchange through an mbarrier instead of bar.sync: a warp
 // arrives when its rows of B are written, forms its Ltilde rows (phase A, which
-// needs only 1/J at the cubature) and then waits for the other warps' rows
+// needs only 1/J at the cubature) and then waits for the other warps' rows.
+// Measured (profiles/round2_mbar_ab.txt): N = 4 / 5 / 6 / 7 -2.1 / -3.5 / -4.0 / -6.3%
+// (Ltilde's accumulators are no longer live across phases D and E: no N = 7 spills)
 #ifndef PDG_WADG_MB
-#define PDG_WADG_MB 0
+#define PDG_WADG_MB 1
 #endif
 #ifndef PDG_WADG_NOEND_MAX_N
 #define PDG_WADG_NOEND_MAX_N 7
