@@ -133,8 +133,11 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #ifndef PDG_MBAR_SYNC_N6
 #define PDG_MBAR_SYNC_N6 0
 #endif
+#ifndef PDG_MBAR_SYNC_N7
+#define PDG_MBAR_SYNC_N7 0
+#endif
 #ifndef PDG_MBAR_SYNC
-#define PDG_MBAR_SYNC(N) ((N) == 5 || ((N) == 6 && PDG_MBAR_SYNC_N6))
+#define PDG_MBAR_SYNC(N) ((N) == 5 || ((N) == 6 && PDG_MBAR_SYNC_N6) || ((N) == 7 && PDG_MBAR_SYNC_N7))
 #endif
 #ifndef PDG_MB_VOL_AFTER
 #define PDG_MB_VOL_AFTER 0
@@ -198,11 +201,15 @@ struct DCfg {
   static constexpr int PER_TEAM = HDR + NSTAGE * STAGE + WORK;
   static constexpr bool NOEND = FBUF == 2 && NSTAGE == 2;
   // mbarrier exchanges need the parity flux buffers (no end-of-element barrier)
-  static constexpr bool MB = PDG_MBAR_SYNC(N) && NOEND && !PDG_SPLIT_ISSUE;
+  // (the V exchange is safe with or without the end-of-element barrier: V of the next
+  // element is written only after its flux exchange, i.e. after every warp has left
+  // this one; the flux exchange needs the parity flux buffers)
+  static constexpr bool MB = PDG_MBAR_SYNC(N) && !PDG_SPLIT_ISSUE; // V exchange
+  static constexpr bool MBF = MB && NOEND;                          // flux exchange
   // measured (profiles/round1_volfirst_ab.txt): N = 4 -2.8%, N = 6 -4.5%, N = 7 -6.5%,
   // N = 5 +0.4% (with the dropped end barrier its gathers are already covered)
   static constexpr bool VF = PDG_VOL_FIRST && (N != 5 || PDG_VF_N5);
-  static constexpr bool VA = MB && !VF && PDG_MB_VOL_AFTER; // volume products after the flux arrival
+  static constexpr bool VA = MBF && !VF && PDG_MB_VOL_AFTER; // volume products after the flux arrival
   static constexpr bool VP = VF || VA;                      // volume products outside G1 / G2
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
   // <= PDG_THREAD_CAP threads per CTA: 384 keeps >= 168 registers per thread
@@ -341,7 +348,7 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
   double* tbase = smem + C::TABLES + (size_t)team * C::PER_TEAM;
   uint64_t* bar = reinterpret_cast<uint64_t*>(tbase);
   double* stg0 = tbase + C::HDR; // 2 mbarriers + 3 schedule slots (+ 2 exchange mbarriers) + pad
-  uint64_t* fbar = bar + 5;      // C::MB: flux exchange
+  uint64_t* fbar = bar + 5;      // C::MBF: flux exchange
   uint64_t* vbar = bar + 6;      // C::MB: V exchange
   double* V = stg0 + NST * C::STAGE;
   double* const Fbase = V + C::VS; // C::FBUF sets of flux buffers (element parity)
@@ -582,7 +589,7 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
         }
       }
     }
-    if (C::MB) {
+    if (C::MBF) {
       mbar_arrive(fbar);
       if (C::VA) volume_products(); // own state only: covers the other warps' fluxes
       mbar_wait(fbar, n & 1);
