@@ -95,6 +95,14 @@ __host__ __device__ constexpr bool tet_tables_global(int N) { return N >= PDG_TE
 #define PDG_TET_END_MBAR 0
 #endif
 
+// gradient products D_a P straight from the staged state (no W columns needed)
+// between issuing the neighbour gathers and using them
+#ifndef PDG_TET_GRAD_FIRST
+#define PDG_TET_GRAD_FIRST 0
+#endif
+// (N = 5, 7 would spill with the gradient accumulators live across the flux phase)
+#define PDG_TET_GF(N) (PDG_TET_GRAD_FIRST && (N) != 5 && (N) != 7)
+
 #ifndef PDG_TET_PAD_STATE
 #define PDG_TET_PAD_STATE 1
 #endif
@@ -315,13 +323,29 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
         const double* Ut = U + t * C::US;
         const double* Gt = G + t * kTG;
         const double ux = Ut[NP + n], uy = Ut[2 * NP + n], uz = Ut[3 * NP + n];
-        BVb[t * VST + n] = Ut[n];
+        if (!PDG_TET_GF(N)) BVb[t * VST + n] = Ut[n];
         BVb[(kTB + t) * VST + n] = Gt[T_RX] * ux + Gt[T_RY] * uy + Gt[T_RZ] * uz;
         BVb[(2 * kTB + t) * VST + n] = Gt[T_SX] * ux + Gt[T_SY] * uy + Gt[T_SZ] * uz;
         BVb[(3 * kTB + t) * VST + n] = Gt[T_TX] * ux + Gt[T_TY] * uy + Gt[T_TZ] * uz;
       }
     }
     };
+    double gr[2] = {0.0, 0.0}, gs[2] = {0.0, 0.0}, gt[2] = {0.0, 0.0};
+    auto grad_products = [&]() {
+      if (vol) {
+#pragma unroll
+        for (int s2 = 0; s2 < KS; ++s2) {
+          const int fo = ((w * KS + s2) << 5) + lane;
+          const double ar = tab(sD, fo), as = tab(sD, C::DTAB + fo), at = tab(sD, 2 * C::DTAB + fo);
+          // B(k = node, n = tet gid) from the tet's state slot (zero A beyond NP)
+          const double bp = U[gid * C::US + 4 * s2 + tig];
+          dmma(gr, ar, bp);
+          dmma(gs, as, bp);
+          dmma(gt, at, bp);
+        }
+      }
+    };
+    if (PDG_TET_GF(N) && !surf) grad_products();
     // ---- fluxes of the batch (scaled by J_f / J) and the W_a columns ------------
     if (kBvFirst && !surf) {
       end_wait();
@@ -356,6 +380,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
           }
         }
       }
+      if (PDG_TET_GF(N)) grad_products(); // own state only, while the gathers are in flight
       end_wait();
       if (kBvFirst) build_bv(); // shared-memory work while the gathers are in flight
 #pragma unroll
@@ -395,7 +420,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
     team_sync(bar_id, 32 * T);
 
     // ---- row tile w: volume and lift products -------------------------------------
-    double gr[2] = {0.0, 0.0}, gs[2] = {0.0, 0.0}, gt[2] = {0.0, 0.0}, dv[2] = {0.0, 0.0};
+    double dv[2] = {0.0, 0.0};
     double lp[2] = {0.0, 0.0}, lu[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
     if (vol) {
 #pragma unroll
@@ -403,8 +428,12 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
         const int fo = ((w * KS + s2) << 5) + lane;
         const double ar = tab(sD, fo), as = tab(sD, C::DTAB + fo), at = tab(sD, 2 * C::DTAB + fo);
         const int bo = gid * VST + 4 * s2 + tig;
-        const double bp = BVb[bo];
-        if (PDG_TET_ORDER == 1) {
+        const double bp = PDG_TET_GF(N) ? 0.0 : BVb[bo];
+        if (PDG_TET_GF(N)) {
+          dmma(dv, ar, BVb[kTB * VST + bo]);
+          dmma(dv, as, BVb[2 * kTB * VST + bo]);
+          dmma(dv, at, BVb[3 * kTB * VST + bo]);
+        } else if (PDG_TET_ORDER == 1) {
           dmma(gr, ar, bp);
           dmma(dv, ar, BVb[kTB * VST + bo]);
           dmma(gs, as, bp);

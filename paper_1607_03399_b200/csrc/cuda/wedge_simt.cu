@@ -114,6 +114,14 @@ __host__ __device__ constexpr int slot_stride(int x, int NT, int H) {
 #define PDG_SIMT_L2_PREFETCH 0
 #endif
 
+// exact mode: the flux exchange of the chunk through an mbarrier -- a thread arrives
+// when its flux tasks are in shared memory, runs the flux-free part of its work
+// (vertical derivative of V, the gradient / divergence / L P products) and only
+// then waits for the other threads' fluxes
+#ifndef PDG_SIMT_MB
+#define PDG_SIMT_MB 0
+#endif
+
 template <int N, bool WADG = false>
 struct SCfg {
   static_assert(nts_of(N) == nt_of(N), "the low-order kernel assumes an unpadded slice stride");
@@ -136,7 +144,7 @@ struct SCfg {
   // exact: Dr^T, Ds^T; WADG adds kd_m^T [m][k][i], Pw^T [q][i], Vq [q][k], R [m][f][a][i], qr, qs
   static constexpr int WTAB = WADG ? 6 * NT * NT + 2 * NC * NT + 6 * NQ * NT + 2 * NC : 0;
   static constexpr int TABLES = r2(r2(2 * NT * NT + NQ * NQ + 2 * NQ + WTAB) + ceil_div(FW, 2) + 2048 / 2);
-  static constexpr size_t SMEM_BYTES = (size_t)8 * (TABLES + 2 * STAGE + E * (SF + SV) + 4);
+  static constexpr size_t SMEM_BYTES = (size_t)8 * (TABLES + 2 * STAGE + E * (SF + SV) + 6); // + slots, mbarrier
   static constexpr int TASKS = ceil_div(E * FW, THREADS);
   // measured (profiles/round1_simt_noend_ab.txt): exact N = 1 -5.5%, N = 3 -1.8%,
   // N = 2 +1%; WADG N = 2 -4.1%, N = 3 -5.2%, N = 1 +2.5%
@@ -199,6 +207,8 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, WADG ? PDG_WADG_SIMT_M
   double* sF = stg + 2 * C::STAGE;     // per wedge fluxes
   double* sV = sF + E * SF;            // per wedge V
   volatile long long* slot = reinterpret_cast<volatile long long*>(sV + E * SV);
+  constexpr bool MBS = PDG_SIMT_MB && !WADG;
+  uint64_t* fxbar = reinterpret_cast<uint64_t*>(sV + E * SV + 4); // MBS: flux exchange
   for (int q = threadIdx.x; q < NT * NT; q += C::THREADS) {
     sDrT[q] = p.DrT[q];
     sDsT[q] = p.DsT[q];
@@ -243,6 +253,10 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, WADG ? PDG_WADG_SIMT_M
     return (int)(r < E ? r : E);
   };
   if (threadIdx.x == 0) {
+    if (MBS) {
+      mbar_init(fxbar, C::THREADS);
+      fence_barrier_init();
+    }
     slot[0] = (long long)(atomicAdd(p.ticket, 1ULL) - p.ticket_base);
     slot[1] = (long long)(atomicAdd(p.ticket, 1ULL) - p.ticket_base);
   }
@@ -400,37 +414,48 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, WADG ? PDG_WADG_SIMT_M
         const double* Ge = sG + e * SG;
         sV[e * SV + 4 * NQ * NT + qq] = 1.0 / (Ge[w_jac(N)] + Ge[w_jac(N) + 1] * sQr[qq] + Ge[w_jac(N) + 2] * sQs[qq]);
       }
-    __syncthreads();
+    if (MBS)
+      mbar_arrive(fxbar);
+    else
+      __syncthreads();
     if constexpr (!WADG) {
     // ---- V column i, gradients, L products, quad lifts (own slices j = h + H jj) -------
     double rp[JH], rux[JH], ruy[JH], ruz[JH], lp[JH];
-    double lf0 = 0.0, lf1 = 0.0;
+    double lf0 = 0.0, lf1 = 0.0, dV[JH];
 #pragma unroll
     for (int jj = 0; jj < JH; ++jj) rp[jj] = rux[jj] = ruy[jj] = ruz[jj] = lp[jj] = 0.0;
+    // V column i: the vertical derivative dV plus the bottom / top pressure lifts
+    auto write_V = [&]() {
+      const double* Fe = sF + el * SF;
+      const double jfb = G[W_JFB], jft = G[W_JFT];
+      const double fb = surf ? jfb * Fe[i] : 0.0, ftop = surf ? jft * Fe[NT + i] : 0.0;
+      double* Ve = sV + el * SV;
+#pragma unroll
+      for (int jj = 0; jj < JH; ++jj) {
+        const int j = h + H * jj;
+        if (j < NQ) Ve[j * NT + i] = -dV[jj] + fb * sProf[j] + ftop * sProf[NQ + j];
+      }
+    };
     if (active) {
       const double* Fe = sF + el * SF;
       const double tzJ = G[W_TZJ], jfb = G[W_JFB], jft = G[W_JFT];
       {
-        const double fb = surf ? jfb * Fe[i] : 0.0, ftop = surf ? jft * Fe[NT + i] : 0.0;
-        double* Ve = sV + el * SV;
 #pragma unroll
         for (int jj = 0; jj < JH; ++jj) {
           const int j = h + H * jj;
-          if (j < NQ) {
-            double d = 0.0;
-            if (vol) {
-              const double sx_ = G[W_TXJ + j], sy_ = G[w_tyj(N) + j];
+          dV[jj] = 0.0;
+          if (j < NQ && vol) {
+            const double sx_ = G[W_TXJ + j], sy_ = G[w_tyj(N) + j];
 #pragma unroll
-              for (int l = 0; l < NQ; ++l) {
-                const double dt = sDt[j * NQ + l];
-                d += U[NP + l * NT + i] * (sx_ * dt);
-                d += U[2 * NP + l * NT + i] * (sy_ * dt);
-                d += U[3 * NP + l * NT + i] * (tzJ * dt);
-              }
+            for (int l = 0; l < NQ; ++l) {
+              const double dt = sDt[j * NQ + l];
+              dV[jj] += U[NP + l * NT + i] * (sx_ * dt);
+              dV[jj] += U[2 * NP + l * NT + i] * (sy_ * dt);
+              dV[jj] += U[3 * NP + l * NT + i] * (tzJ * dt);
             }
-            Ve[j * NT + i] = -d + fb * sProf[j] + ftop * sProf[NQ + j];
           }
         }
+        if (!MBS) write_V();
       }
       const double rx = G[W_RX], ry = G[W_RY], sxm = G[W_SX], sym = G[W_SY];
 #pragma unroll
@@ -455,11 +480,28 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, WADG ? PDG_WADG_SIMT_M
             }
           }
         }
-        if (surf) {
+        if (surf && !MBS) {
           lf0 += lk * Fe[2 * NT + k];
           lf1 += lk * Fe[3 * NT + k];
         }
       }
+    }
+    if (MBS) {
+      mbar_wait(fxbar, it & 1); // every thread's fluxes of the chunk are in
+      if (active) {
+        write_V();
+        if (surf) {
+          const double* Fe = sF + el * SF;
+#pragma unroll
+          for (int k = 0; k < NT; ++k) {
+            lf0 += Lr[k] * Fe[2 * NT + k];
+            lf1 += Lr[k] * Fe[3 * NT + k];
+          }
+        }
+      }
+    }
+    if (active) {
+      const double* Fe = sF + el * SF;
       if (surf) {
         const double* QL = p.QL + ge * qcomp_of(N) + i;
         const double* nrm = G + w_nrm(N);
