@@ -84,15 +84,17 @@ __host__ __device__ constexpr bool tet_tables_global(int N) { return N >= PDG_TE
 // rewritten only after every thread has read it, so the barrier that protected
 // the single slot goes (two team barriers per batch instead of three)
 #ifndef PDG_TET_SLOT_PARITY
-#define PDG_TET_SLOT_PARITY 0
+#define PDG_TET_SLOT_PARITY 1
 #endif
 
 // end-of-batch barrier through an mbarrier (needs the slot parity and two stages):
 // a warp arrives when it has finished the batch and only waits for the others
 // right before it writes the work buffers of the next batch (after issuing that
-// batch's neighbour gathers); thread 0 refills the freed stage after that wait
+// batch's neighbour gathers); thread 0 refills the freed stage after that wait.
+// Measured with the slot parity (profiles/round2_mbar_ab.txt): N = 3 / 4 / 5
+// -3.5 / -2.8 / -4.7% (slot parity alone: +0.2 / -0.6 / -0.1%)
 #ifndef PDG_TET_END_MBAR
-#define PDG_TET_END_MBAR 0
+#define PDG_TET_END_MBAR 1
 #endif
 
 // gradient products D_a P straight from the staged state (no W columns needed)

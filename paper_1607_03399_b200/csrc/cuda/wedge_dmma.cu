@@ -82,8 +82,10 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #ifndef PDG_VOL_FIRST
 #define PDG_VOL_FIRST 1
 #endif
+// at N = 5 volume-first was +0.4% with bar.sync exchanges (round 1) and is -0.6%
+// with the mbarrier exchanges (profiles/round2_mbar_ab.txt)
 #ifndef PDG_VF_N5
-#define PDG_VF_N5 0
+#define PDG_VF_N5 1
 #endif
 // k permutation of the triangle products (G2/G3) at odd NT: in every block of four
 // k-steps lane (gid, tig) takes k = 16 b + 4 tig + s instead of 4 s + tig, so the
@@ -207,7 +209,7 @@ struct DCfg {
   static constexpr bool MB = PDG_MBAR_SYNC(N) && !PDG_SPLIT_ISSUE; // V exchange
   static constexpr bool MBF = MB && NOEND;                          // flux exchange
   // measured (profiles/round1_volfirst_ab.txt): N = 4 -2.8%, N = 6 -4.5%, N = 7 -6.5%,
-  // N = 5 +0.4% (with the dropped end barrier its gathers are already covered)
+  // N = 5 +0.4% before the mbarrier exchanges, -0.6% with them (PDG_VF_N5)
   static constexpr bool VF = PDG_VOL_FIRST && (N != 5 || PDG_VF_N5);
   static constexpr bool VA = MBF && !VF && PDG_MB_VOL_AFTER; // volume products after the flux arrival
   static constexpr bool VP = VF || VA;                      // volume products outside G1 / G2
