@@ -105,6 +105,12 @@ __host__ __device__ constexpr bool tet_tables_global(int N) { return N >= PDG_TE
 // (N = 5, 7 would spill with the gradient accumulators live across the flux phase)
 #define PDG_TET_GF(N) (PDG_TET_GRAD_FIRST && (N) != 5 && (N) != 7)
 
+// the next batch index published just before the flux barrier instead of right after
+// the ticket atomic, so the atomic's round trip overlaps the gathers and fluxes
+#ifndef PDG_TET_LATE_SLOT
+#define PDG_TET_LATE_SLOT 0
+#endif
+
 #ifndef PDG_TET_PAD_STATE
 #define PDG_TET_PAD_STATE 1
 #endif
@@ -275,7 +281,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
     long long bn = 0;
     if (tt == 0) {
       bn = grab();
-      slot[PDG_TET_SLOT_PARITY ? 1 + (it & 1) : 1] = bn;
+      if (!(PDG_TET_LATE_SLOT && PDG_TET_SLOT_PARITY)) slot[PDG_TET_SLOT_PARITY ? 1 + (it & 1) : 1] = bn;
     }
     const double* U = stg0 + s * C::STAGE;
     const double* G = U + C::UB;
@@ -419,6 +425,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
     end_wait();
     if (!kBvFirst) build_bv();
     if (PDG_TET_RES_LATE) load_res();
+    if (PDG_TET_LATE_SLOT && PDG_TET_SLOT_PARITY && tt == 0) slot[1 + (it & 1)] = bn; // read after the barrier
     team_sync(bar_id, 32 * T);
 
     // ---- row tile w: volume and lift products -------------------------------------

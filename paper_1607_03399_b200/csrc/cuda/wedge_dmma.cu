@@ -141,6 +141,12 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #ifndef PDG_MBAR_SYNC
 #define PDG_MBAR_SYNC(N) ((N) == 5 || ((N) == 6 && PDG_MBAR_SYNC_N6) || ((N) == 7 && PDG_MBAR_SYNC_N7))
 #endif
+// with the mbarrier exchanges the grabber publishes the next element index after the
+// flux exchange (the V exchange orders it before every reader), so the ticket
+// atomic's round trip overlaps the gathers and the flux phase
+#ifndef PDG_MB_LATE_SLOT
+#define PDG_MB_LATE_SLOT 0
+#endif
 #ifndef PDG_MB_VOL_AFTER
 #define PDG_MB_VOL_AFTER 0
 #endif
@@ -485,7 +491,8 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
     long long en = 0;
     if (grabber) {
       en = grab();
-      slot[1 + (n & 1)] = en; // parity slots: rewritten only after every thread read it
+      if (!(C::MBF && PDG_MB_LATE_SLOT))
+        slot[1 + (n & 1)] = en; // parity slots: rewritten only after every thread read it
     }
     const double* U = stg0 + s * C::STAGE;
     const double* R = U + C::USTR;
@@ -595,6 +602,7 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
       mbar_arrive(fbar);
       if (C::VA) volume_products(); // own state only: covers the other warps' fluxes
       mbar_wait(fbar, n & 1);
+      if (PDG_MB_LATE_SLOT && grabber) slot[1 + (n & 1)] = en; // read after the V exchange
     } else {
       team_sync(bar_id, 32 * T);
     }
@@ -748,9 +756,9 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
             }
           }
       }
+      if (C::MB) mbar_wait(vbar, n & 1); // every warp's V rows (and the next element index) are in
       if (C::MB && !PDG_MEMONLY) {
-        // L V once every warp's V rows are in
-        mbar_wait(vbar, n & 1);
+        // L V
 #pragma unroll
         for (int s2 = 0; s2 < KS; ++s2) {
           const int k = kmap(s2, tig, KS, C::KP);

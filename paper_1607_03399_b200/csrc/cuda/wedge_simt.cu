@@ -117,9 +117,10 @@ __host__ __device__ constexpr int slot_stride(int x, int NT, int H) {
 // exact mode: the flux exchange of the chunk through an mbarrier -- a thread arrives
 // when its flux tasks are in shared memory, runs the flux-free part of its work
 // (vertical derivative of V, the gradient / divergence / L P products) and only
-// then waits for the other threads' fluxes
+// then waits for the other threads' fluxes.  Bitwise the same results; measured
+// (profiles/round2_mbar_ab.txt) N = 1 / 2 / 3: 0 / -1.5 / -0.6%
 #ifndef PDG_SIMT_MB
-#define PDG_SIMT_MB 0
+#define PDG_SIMT_MB 1
 #endif
 
 template <int N, bool WADG = false>
