@@ -141,9 +141,10 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #ifndef PDG_MBAR_SYNC
 #define PDG_MBAR_SYNC(N) ((N) == 5 || ((N) == 6 && PDG_MBAR_SYNC_N6) || ((N) == 7 && PDG_MBAR_SYNC_N7))
 #endif
-// with the mbarrier exchanges the grabber publishes the next element index after the
-// flux exchange (the V exchange orders it before every reader), so the ticket
-// atomic's round trip overlaps the gathers and the flux phase
+// the grabber publishes the next element index at the flux exchange instead of right
+// after the ticket atomic (with the mbarrier exchanges after the flux wait, the V
+// exchange ordering it before every reader; with bar.sync just before the flux
+// barrier), so the atomic's round trip overlaps the gathers and the flux phase
 #ifndef PDG_MB_LATE_SLOT
 #define PDG_MB_LATE_SLOT 0
 #endif
@@ -491,7 +492,7 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
     long long en = 0;
     if (grabber) {
       en = grab();
-      if (!(C::MBF && PDG_MB_LATE_SLOT))
+      if (!PDG_MB_LATE_SLOT || SPLIT)
         slot[1 + (n & 1)] = en; // parity slots: rewritten only after every thread read it
     }
     const double* U = stg0 + s * C::STAGE;
@@ -604,6 +605,7 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
       mbar_wait(fbar, n & 1);
       if (PDG_MB_LATE_SLOT && grabber) slot[1 + (n & 1)] = en; // read after the V exchange
     } else {
+      if (PDG_MB_LATE_SLOT && !SPLIT && grabber) slot[1 + (n & 1)] = en; // read after the barrier
       team_sync(bar_id, 32 * T);
     }
     // every warp of the team has left the previous element: its stage may be refilled

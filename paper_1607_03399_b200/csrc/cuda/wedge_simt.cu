@@ -118,9 +118,13 @@ __host__ __device__ constexpr int slot_stride(int x, int NT, int H) {
 // when its flux tasks are in shared memory, runs the flux-free part of its work
 // (vertical derivative of V, the gradient / divergence / L P products) and only
 // then waits for the other threads' fluxes.  Bitwise the same results; measured
-// (profiles/round2_mbar_ab.txt) N = 1 / 2 / 3: 0 / -1.5 / -0.6%
+// (profiles/round2_mbar_ab.txt) N = 1 / 2: -0.3 / -0.3..-1.5%; N = 3 -0.7% and +3.5%
+// on two boxes, so on at N <= 2 only
 #ifndef PDG_SIMT_MB
 #define PDG_SIMT_MB 1
+#endif
+#ifndef PDG_SIMT_MB_MAXN
+#define PDG_SIMT_MB_MAXN 2
 #endif
 
 template <int N, bool WADG = false>
@@ -208,7 +212,7 @@ __global__ void __launch_bounds__(SCfg<N, WADG>::THREADS, WADG ? PDG_WADG_SIMT_M
   double* sF = stg + 2 * C::STAGE;     // per wedge fluxes
   double* sV = sF + E * SF;            // per wedge V
   volatile long long* slot = reinterpret_cast<volatile long long*>(sV + E * SV);
-  constexpr bool MBS = PDG_SIMT_MB && !WADG;
+  constexpr bool MBS = PDG_SIMT_MB && !WADG && N <= PDG_SIMT_MB_MAXN;
   uint64_t* fxbar = reinterpret_cast<uint64_t*>(sV + E * SV + 4); // MBS: flux exchange
   for (int q = threadIdx.x; q < NT * NT; q += C::THREADS) {
     sDrT[q] = p.DrT[q];
