@@ -79,6 +79,14 @@ def wadg_flops_per_wedge_stage(N):
             + 2 * nt * nt * 4 * nq)
 
 
+def tet_flops_per_stage(N):
+    """algorithmic FP64 flops of the tet stage kernel per tet: gradients
+    D_a P and divergence sum_a D_a W_a (6 NP x NP products), the W_a columns, and the
+    four face lifts of the p and u fluxes (8 NP x NT products)."""
+    np_, nt = (N + 1) * (N + 2) * (N + 3) // 6, (N + 1) * (N + 2) // 2
+    return 12 * np_ * np_ + 3 * 5 * np_ + 16 * np_ * nt
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -319,6 +327,17 @@ def measure_degree(args, degree, ws, rank, local, peaks, with_e2e=True):
         res["tet_roofline"] = {"bound": "hbm", "achieved": t_ach, "peak": peaks[0], "unit": "GB/s",
                                "frac": t_ach / peaks[0], "peak_source": peaks[1],
                                "traffic": load_traffic("tet", degree), "algorithmic_bytes": tbytes}
+        # at high N the tet stage is FP64 tensor work (dense NP x NP operators): its
+        # roofline against the DMMA peak (N = 8, 9 run on the FP64 CUDA cores)
+        tfl = tet_flops_per_stage(degree) * mesh.num_tets()
+        tsimt = degree >= 8
+        tpk = DFMA_PEAK_TFLOPS if tsimt else DMMA_PEAK_TFLOPS
+        res["tet_tensor_roofline"] = {"bound": "fp64" if tsimt else "tensor",
+                                      "achieved": tfl / (tet_avg_ms / 1e3) / 1e12, "peak": tpk, "unit": "TFLOP/s",
+                                      "frac": tfl / (tet_avg_ms / 1e3) / 1e12 / tpk,
+                                      "peak_source": ("FP64 FMA" if tsimt else "FP64 mma.sync m8n8k4 (DMMA)") +
+                                                     ", scripts/micro/dmma_bench.cu on this pool",
+                                      "flops_per_launch": tfl}
     if with_e2e:
         # e2e through the C ABI: pinned host state in, one step, state out, every step
         host = torch.empty(dofs, dtype=torch.float64, pin_memory=True)
@@ -578,7 +597,7 @@ def main():
         r = measure_degree(args, deg, ws, rank, local, peaks, with_e2e=False)
         sweep.append({k: r[k] for k in ("degree", "value", "ms_per_step", "wedge_kernel_avg_ms", "roofline",
                                         "total_dofs", "setup_s", "gpu_launches", "tensor_roofline",
-                                        "tet_kernel_avg_ms", "tet_roofline") if k in r})
+                                        "tet_kernel_avg_ms", "tet_roofline", "tet_tensor_roofline") if k in r})
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -607,7 +626,8 @@ def main():
             **({"e2e_run_simulation": head["e2e_run_simulation"]} if "e2e_run_simulation" in head else {}),
             "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
             "wedge_kernel_avg_ms": head["wedge_kernel_avg_ms"], "wedge_kernel_share": head["wedge_kernel_share"],
-            **({k: head[k] for k in ("tet_kernel_avg_ms", "tet_kernel_share", "tet_roofline", "tensor_roofline")
+            **({k: head[k] for k in ("tet_kernel_avg_ms", "tet_kernel_share", "tet_roofline", "tet_tensor_roofline",
+                                       "tensor_roofline")
                 if k in head}),
             "setup_s": head["setup_s"],
         }
