@@ -1,6 +1,6 @@
 #!/bin/bash
-# late round-2 measurement set on the final kernels: GPU suite, smoke, default bench (N=5 + N=1..7 sweep),
-# reference arm, WADG and hybrid sweeps, ncu launch list, ncu --set full per N (wedge), tet N=4, WADG N=5
+# late round-2 measurement set (small outputs): reference arm, default bench (N=5 + N=1..7 sweep), WADG and
+# hybrid sweeps, GPU suite, smoke, ncu launch list
 cd "$GRAFT_REPO_ROOT" || exit 1
 tag=${1:-m2}
 nvidia-smi -q -d CLOCK,POWER > gpurun_out/${tag}_smi.txt 2>&1
@@ -14,14 +14,3 @@ timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${ta
 echo "rc=$?" >> gpurun_out/${tag}_smoke.log
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_launches_n5.csv \
   python bench.py --steps 2 --warmup 3 --degrees "" --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
-for n in 1 2 3 4 5 6 7; do
-  timeout 900 ncu --set full --import-source on --clock-control none -k regex:wedge_ -s 16 -c 1 \
-    -o gpurun_out/${tag}_full_n${n} -f python bench.py --steps 1 --warmup 3 --degree $n --degrees "" \
-    --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
-done
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:tet_dmma -s 8 -c 1 \
-  -o gpurun_out/${tag}_tet4 -f python bench.py --steps 1 --warmup 3 --workload hybrid --degree 4 --degrees "" \
-  --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:wedge_wadg -s 16 -c 1 \
-  -o gpurun_out/${tag}_wadg5 -f python bench.py --steps 1 --warmup 3 --mass wadg --degree 5 --degrees "" \
-  --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
