@@ -160,6 +160,19 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #define PDG_FU_DOT 0
 #endif
 
+// N = 6: the [P | Fu0 | Fu1] product's second tile holds only Fu1; instead Fu1
+// rides in the free padding column NQ of the V operand, so L Fu1 comes out of the
+// L V product and the second tile's DMMAs go (KS per warp and element)
+#ifndef PDG_FU1_IN_V
+#define PDG_FU1_IN_V 0
+#endif
+
+// the epilogue's 15 face normals read as 16-byte pairs (8 shared loads per lane
+// instead of 15; the record is 16-byte aligned in the stage)
+#ifndef PDG_NRM_VEC
+#define PDG_NRM_VEC 0
+#endif
+
 /// k index of lane column tig in k-step s (see PDG_KPERM)
 __host__ __device__ constexpr int kmap(int s, int tig, int KS, bool perm) {
   return (perm && s < 4 * (KS / 4)) ? 16 * (s >> 2) + 4 * tig + (s & 3) : 4 * s + tig;
@@ -173,7 +186,9 @@ struct DCfg {
   static constexpr int JT = ceil_div(NQ, 8), NPJ = 8 * JT;   // slice column tiles
   static constexpr int JTL = ceil_div(NQ + 2, 8);            // [P | Fu0 | Fu1] tiles
   static constexpr bool FUV = PDG_FU_DOT && 8 * (JTL - 1) >= NQ; // last tile = fluxes only
-  static constexpr int JL = FUV ? JTL - 1 : JTL;               // tiles on the tensor cores
+  // Fu1 alone in the last tile, and L V complete before the epilogue setup (no deferred L V)
+  static constexpr bool F1V = PDG_FU1_IN_V && !FUV && NQ + 1 == 8 * JT && !(PDG_MBAR_SYNC(N) && !PDG_SPLIT_ISSUE);
+  static constexpr int JL = (FUV || F1V) ? JTL - 1 : JTL;      // tiles on the tensor cores
   static constexpr bool DOT0 = FUV && NQ >= 8 * (JTL - 1);     // Fu0 in the last tile too
   static constexpr int T = IT;                               // warps per team
   // per-wedge operator block sizes in HBM / the stage buffer
@@ -648,6 +663,7 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
           if (i < NT && j < NQ) V[j * VST + i] = -d[c] + fb * sProf[j] + ftop * sProf[NQ + j];
         }
       }
+      if (C::F1V && tig == 0 && i < NT) V[NQ * VST + i] = surf ? Ftu[NT + i] : 0.0; // column NQ: Fu1
     }
     if (C::MB)
       mbar_arrive(vbar); // L V waits for it after the V-independent products
@@ -730,7 +746,10 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
         d1 += __shfl_xor_sync(0xffffffffu, d1, 2);
       }
       const double lf0 = C::DOT0 ? d0 : __shfl_sync(0xffffffffu, lp[NQ / 8][c0 & 1], gid * 4 + c0 / 2);
-      const double lf1 = C::FUV ? d1 : __shfl_sync(0xffffffffu, lp[(NQ + 1) / 8][c1 & 1], gid * 4 + c1 / 2);
+      constexpr int cv = NQ - 8 * (JT - 1); // C::F1V: column of L Fu1 in the last L V tile
+      const double lf1 = C::FUV ? d1
+                         : C::F1V ? __shfl_sync(0xffffffffu, lv[JT - 1][cv & 1], gid * 4 + cv / 2)
+                                  : __shfl_sync(0xffffffffu, lp[(NQ + 1) / 8][c1 & 1], gid * 4 + c1 / 2);
       // G5: quad-face lifts; the velocity lift of each face is kept separately
       // and scaled by that face's normal in the epilogue
       double qp[JT][2], qu[3][JT][2];
@@ -778,10 +797,24 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
       const double kappa = G[W_KAPPA], irho = G[W_IRHO];
       const double pa = p.a, pb = p.b, pdt = p.dt;
       double n_[5][3];
+      if (PDG_NRM_VEC) {
+        constexpr int nb = w_nrm(N) & ~1, nv = (w_nrm(N) + 15 - nb + 1) / 2;
+        double2 pr[nv];
 #pragma unroll
-      for (int f = 0; f < 5; ++f)
+        for (int v = 0; v < nv; ++v) pr[v] = *reinterpret_cast<const double2*>(G + nb + 2 * v);
 #pragma unroll
-        for (int a = 0; a < 3; ++a) n_[f][a] = nrm[3 * f + a];
+        for (int f = 0; f < 5; ++f)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const int o = w_nrm(N) + 3 * f + a - nb;
+            n_[f][a] = (o & 1) ? pr[o >> 1].y : pr[o >> 1].x;
+          }
+      } else {
+#pragma unroll
+        for (int f = 0; f < 5; ++f)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) n_[f][a] = nrm[3 * f + a];
+      }
       // per-lane base offset of position (i, j = 2 tig); (jt, c, field) add constants
       const int lane_off = 2 * tig * ST + i;
       const double* Ul = Us + 2 * tig * SP + i; // padded rows: (field*NQ + j)*SP + i
