@@ -88,8 +88,11 @@ __host__ __device__ constexpr int slot_stride(int x, int NT, int H) {
 // threads per (wedge, triangle node) in exact mode: 2 halves the per-thread
 // slice arrays (registers) and the chunk, so more CTAs are resident.  Measured
 // faster at N = 1 only (-6%; +18% at N = 2, 3), profiles/round1_simt_variants_ab.txt
+#ifndef PDG_SIMT_SPLIT_MAXN
+#define PDG_SIMT_SPLIT_MAXN 1
+#endif
 #ifndef PDG_SIMT_SPLIT
-#define PDG_SIMT_SPLIT(N) ((N) == 1 ? 2 : 1)
+#define PDG_SIMT_SPLIT(N) ((N) <= PDG_SIMT_SPLIT_MAXN ? 2 : 1)
 #endif
 #ifndef PDG_SIMT_MINB
 #ifdef PDG_SIMT_MINB_ALL
