@@ -158,6 +158,19 @@ bool use_wedge_lo(int N) {
   return wedge_lo_supported(N) && env != 0 && (env > 0 || PDG_WEDGE_LO_DEFAULT);
 }
 
+// exact-mode wedge kernel at N = 1: the thread-per-(wedge, slice) kernel (wedge_sl.cu)
+// when PDG_WEDGE_SL=1 (or PDG_WEDGE_SL_DEFAULT)
+#ifndef PDG_WEDGE_SL_DEFAULT
+#define PDG_WEDGE_SL_DEFAULT 0
+#endif
+bool use_wedge_sl(int N) {
+  static const int env = [] {
+    const char* v = std::getenv("PDG_WEDGE_SL");
+    return v ? std::atoi(v) : -1;
+  }();
+  return wedge_sl_supported(N) && env != 0 && (env > 0 || PDG_WEDGE_SL_DEFAULT);
+}
+
 void launch_checked(pdg_ctx* c, const StageParams& p0, bool wedge) {
   cudaEvent_t a = nullptr, b = nullptr;
   if (c->flags & 2) {
@@ -171,8 +184,9 @@ void launch_checked(pdg_ctx* c, const StageParams& p0, bool wedge) {
   cudaError_t err = !wedge ? launch_tet_stage(c->N, p, c->stream)
                     : c->wadg ? (c->N <= wedge_wadg_simt_max_degree() ? launch_wedge_wadg_simt_stage(c->N, p, c->stream)
                                                                      : launch_wedge_wadg_stage(c->N, p, c->stream))
-                    : c->wedge_simt ? (use_wedge_lo(c->N) ? launch_wedge_lo_stage(c->N, p, c->stream)
-                                                          : launch_wedge_simt_stage(c->N, p, c->stream))
+                    : c->wedge_simt ? (use_wedge_sl(c->N)   ? launch_wedge_sl_stage(c->N, p, c->stream)
+                                       : use_wedge_lo(c->N) ? launch_wedge_lo_stage(c->N, p, c->stream)
+                                                            : launch_wedge_simt_stage(c->N, p, c->stream))
                     : use_wedge_ws(c->N) ? launch_wedge_ws_stage(c->N, p, c->stream)
                                          : launch_wedge_stage(c->N, p, c->stream);
   if (err != cudaSuccess) {

@@ -186,6 +186,9 @@ int wedge_simt_max_degree();
 /// thread-per-DOF-column low-order exact wedge kernel (wedge_lo.cu, N = 1..3)
 bool wedge_lo_supported(int N);
 cudaError_t launch_wedge_lo_stage(int N, const StageParams& p, cudaStream_t s);
+/// thread-per-(wedge, slice) exact wedge kernel (wedge_sl.cu, N = 1)
+bool wedge_sl_supported(int N);
+cudaError_t launch_wedge_sl_stage(int N, const StageParams& p, cudaStream_t s);
 cudaError_t launch_wedge_simt_stage(int N, const StageParams& p, cudaStream_t s); // low-order CUDA-core wedge kernel
 int wedge_wadg_simt_max_degree();
 cudaError_t launch_wedge_wadg_simt_stage(int N, const StageParams& p, cudaStream_t s); // low-order WADG
