@@ -35,6 +35,9 @@ namespace pdg {
 namespace {
 
 __host__ __device__ constexpr int r2(int x) { return (x + 1) & ~1; }
+/// smallest slot stride >= x that is 2 mod 16 (doubles): the 16 wedges of a warp read
+/// their slots on 8 distinct bank pairs (2 mod 16 is the best an even stride can do)
+__host__ __device__ constexpr int slot16(int x) { return x % 16 == 2 ? x : slot16(x + 1); }
 
 #ifndef PDG_SL_THREADS
 #define PDG_SL_THREADS 128
@@ -55,7 +58,7 @@ struct SLCfg {
   // exact mode reads the record up to the WADG fields (w_jac), so only that part is copied
   static constexpr int WGX = w_jac(N);
   static_assert(WGX % 2 == 0, "16-byte copies of the record");
-  static constexpr int SW = SU + LF + QF + WGX + kWC / 2; // per-wedge slot: U | L | QL | record | connectivity
+  static constexpr int SW = slot16(SU + LF + QF + WGX + kWC / 2); // per-wedge slot: U | L | QL | record | connectivity
   static constexpr int STAGE = E * SW;
   static constexpr int TABLES = r2(r2(2 * NT * NT + NQ * NQ + 2 * NQ) + ceil_div(FW, 2) + 2048 / 2);
   static constexpr size_t SMEM_BYTES = (size_t)8 * (TABLES + 2 * STAGE + 4);
@@ -69,39 +72,33 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-/// copy state, L, quad lifts, record and connectivity of wedges [e0, e0 + nel) into the stage
+/// the wedge's NQ threads copy its state, L, quad lifts, record and connectivity into
+/// its slot (thread j takes vectors j, j + NQ, ...: compile-time offsets, no division)
 template <int N>
-__device__ __forceinline__ void sl_load_chunk(const StageParams& p, double* stg, long long e0, int nel) {
+__device__ __forceinline__ void sl_load_wedge(const StageParams& p, double* slot, long long ge, int j) {
   using C = SLCfg<N>;
+  constexpr int NQ = C::NQ;
   constexpr int UV = 2 * C::NP, LV = C::LF / 2, QV = C::QF / 2, GV = C::WGX / 2, CV = kWC / 4;
-  constexpr int PER = UV + LV + QV + GV + CV; // 16-byte vectors per wedge
-  for (int q = threadIdx.x; q < nel * PER; q += C::THREADS) {
-    const int e = q / PER;
-    int v = q - e * PER;
-    double* slot = stg + e * C::SW;
-    const long long ge = e0 + e;
-    if (v < UV) {
-      cp_async16(slot + 2 * v, p.u_in + ge * 4 * C::NP + 2 * v);
-      continue;
-    }
-    v -= UV;
-    if (v < LV) {
-      cp_async16(slot + C::SU + 2 * v, p.Lt + ge * C::LF + 2 * v);
-      continue;
-    }
-    v -= LV;
-    if (v < QV) {
-      cp_async16(slot + C::SU + C::LF + 2 * v, p.QL + ge * C::QF + 2 * v);
-      continue;
-    }
-    v -= QV;
-    if (v < GV) {
-      cp_async16(slot + C::SU + C::LF + C::QF + 2 * v, p.wgeo + ge * C::WG + 2 * v);
-      continue;
-    }
-    v -= GV;
-    cp_async16(slot + C::SU + C::LF + C::QF + C::WGX + 2 * v, p.wconn + ge * kWC + 4 * v);
-  }
+  const double* u = p.u_in + ge * 4 * C::NP;
+  const double* l = p.Lt + ge * C::LF;
+  const double* q = p.QL + ge * C::QF;
+  const double* g = p.wgeo + ge * C::WG;
+  const int* cn = p.wconn + ge * kWC;
+#pragma unroll
+  for (int v = 0; v < UV; v += NQ)
+    if (v + j < UV) cp_async16(slot + 2 * (v + j), u + 2 * (v + j));
+#pragma unroll
+  for (int v = 0; v < LV; v += NQ)
+    if (v + j < LV) cp_async16(slot + C::SU + 2 * (v + j), l + 2 * (v + j));
+#pragma unroll
+  for (int v = 0; v < QV; v += NQ)
+    if (v + j < QV) cp_async16(slot + C::SU + C::LF + 2 * (v + j), q + 2 * (v + j));
+#pragma unroll
+  for (int v = 0; v < GV; v += NQ)
+    if (v + j < GV) cp_async16(slot + C::SU + C::LF + C::QF + 2 * (v + j), g + 2 * (v + j));
+#pragma unroll
+  for (int v = 0; v < CV; v += NQ)
+    if (v + j < CV) cp_async16(slot + C::SU + C::LF + C::QF + C::WGX + 2 * (v + j), cn + 4 * (v + j));
 }
 
 template <int N>
@@ -127,7 +124,6 @@ __global__ void __launch_bounds__(SLCfg<N>::THREADS, PDG_SL_MINB) wedge_sl_kerne
   const bool combo_smem = p.nbr_nodes_len <= 2048;
   if (combo_smem)
     for (int q = threadIdx.x; q < p.nbr_nodes_len; q += C::THREADS) sCombo[q] = p.nbr_nodes[q];
-  const int* combo = combo_smem ? sCombo : p.nbr_nodes;
 
   const int mode = p.mode;
   const bool vol = mode & M_VOLUME, surf = mode & M_SURFACE;
@@ -145,11 +141,10 @@ __global__ void __launch_bounds__(SLCfg<N>::THREADS, PDG_SL_MINB) wedge_sl_kerne
   }
   __syncthreads();
   long long c = slot[0], cn = slot[1];
-  if (c < nchunk) sl_load_chunk<N>(p, stg, p.Kw_begin + c * E, nel_of(c));
-  cp_async_commit();
-
   // this thread: wedge el of the chunk, slice j; lanes lb .. lb + NQ - 1 hold the wedge
   const int el = threadIdx.x / NQ, j = threadIdx.x - el * NQ;
+  if (c < nchunk && el < nel_of(c)) sl_load_wedge<N>(p, stg + el * SW, p.Kw_begin + c * E + el, j);
+  cp_async_commit();
   const int lane = threadIdx.x & 31, lb = lane - j;
   double dtj[NQ];
 #pragma unroll
@@ -166,7 +161,8 @@ __global__ void __launch_bounds__(SLCfg<N>::THREADS, PDG_SL_MINB) wedge_sl_kerne
     if (threadIdx.x == 0) slot[2 + (it & 1)] = (long long)(atomicAdd(p.ticket, 1ULL) - p.ticket_base);
     __syncthreads();
     // every thread has left the previous chunk: its stage takes the one after this
-    if (cn < nchunk) sl_load_chunk<N>(p, stg + ((it + 1) & 1) * C::STAGE, p.Kw_begin + cn * E, nel_of(cn));
+    if (cn < nchunk && el < nel_of(cn))
+      sl_load_wedge<N>(p, stg + ((it + 1) & 1) * C::STAGE + el * SW, p.Kw_begin + cn * E + el, j);
     cp_async_commit();
     const long long e0 = p.Kw_begin + c * E;
     const int nel = nel_of(c);
@@ -184,7 +180,7 @@ __global__ void __launch_bounds__(SLCfg<N>::THREADS, PDG_SL_MINB) wedge_sl_kerne
     for (int f = 0; f < 4; ++f)
 #pragma unroll
       for (int i = 0; i < NT; ++i)
-        rres[f][i] = (active && res_src) ? __ldcs(res_src + ge * 4 * NP + f * NP + j * NT + i) : 0.0;
+        rres[f][i] = (active && res_src) ? __ldg(res_src + ge * 4 * NP + f * NP + j * NT + i) : 0.0;
 
     // ---- fluxes on the slice's face nodes ------------------------------------------
     // tri: [p|u][node], quad: [p|u][face][a]
@@ -204,7 +200,8 @@ __global__ void __launch_bounds__(SLCfg<N>::THREADS, PDG_SL_MINB) wedge_sl_kerne
         const int loc = tri ? q : ((q - NFT) % NQ) * NQ + j;
         const int nbr = Cn[2 * f];
         if (nbr >= 0) {
-          const int node = combo[Cn[2 * f + 1] * p.max_nfp + loc];
+          const int ci = Cn[2 * f + 1] * p.max_nfp + loc;
+          const int node = combo_smem ? sCombo[ci] : __ldg(p.nbr_nodes + ci);
           const double* src;
           int fs;
           if (nbr < p.Kw) {
