@@ -130,8 +130,12 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 // [P | Fu0 | Fu1], LY and the quad-face lifts) run between the V arrival and the
 // V wait, and (PDG_MB_VOL_AFTER, where the volume products are not issued first)
 // the element's volume products between the flux arrival and the flux wait.
-// Measured (profiles/round2_mbar_ab.txt): N = 5 -1.7% (adopted), N = 4 +0.4%;
-// volume products after the flux arrival +1.3% at N = 5 (not adopted)
+// Measured (profiles/round2_mbar_ab.txt): N = 5 -1.7% (adopted), N = 4 +0.4% alone and
+// -1.4% with PDG_MB_LP_LATE (adopted); volume products after the flux arrival +1.3% at
+// N = 5 (not adopted)
+#ifndef PDG_MBAR_SYNC_N4
+#define PDG_MBAR_SYNC_N4 1
+#endif
 #ifndef PDG_MBAR_SYNC_N6
 #define PDG_MBAR_SYNC_N6 0
 #endif
@@ -139,7 +143,8 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #define PDG_MBAR_SYNC_N7 0
 #endif
 #ifndef PDG_MBAR_SYNC
-#define PDG_MBAR_SYNC(N) ((N) == 5 || ((N) == 6 && PDG_MBAR_SYNC_N6) || ((N) == 7 && PDG_MBAR_SYNC_N7))
+#define PDG_MBAR_SYNC(N) \
+  ((N) == 5 || ((N) == 4 && PDG_MBAR_SYNC_N4) || ((N) == 6 && PDG_MBAR_SYNC_N6) || ((N) == 7 && PDG_MBAR_SYNC_N7))
 #endif
 // the grabber publishes the next element index at the flux exchange instead of right
 // after the ticket atomic (with the mbarrier exchanges after the flux wait, the V
@@ -147,6 +152,14 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 // barrier), so the atomic's round trip overlaps the gathers and the flux phase
 #ifndef PDG_MB_LATE_SLOT
 #define PDG_MB_LATE_SLOT 0
+#endif
+// with the mbarrier exchanges and the volume products issued first, the L [P | Fu0 | Fu1]
+// product moves behind the V wait too and shares its L fragments with L V (one
+// L read per element instead of two; only the quad-face lifts cover the V skew)
+// Measured (profiles/round2_mbar_ab.txt): N = 5 -1.1%; with it the mbarrier exchanges
+// pay at N = 4 too (-1.4% together)
+#ifndef PDG_MB_LP_LATE
+#define PDG_MB_LP_LATE 1
 #endif
 #ifndef PDG_MB_VOL_AFTER
 #define PDG_MB_VOL_AFTER 0
@@ -235,6 +248,7 @@ struct DCfg {
   static constexpr bool VF = PDG_VOL_FIRST && (N != 5 || PDG_VF_N5);
   static constexpr bool VA = MBF && !VF && PDG_MB_VOL_AFTER; // volume products after the flux arrival
   static constexpr bool VP = VF || VA;                      // volume products outside G1 / G2
+  static constexpr bool LPL = PDG_MB_LP_LATE && MB && VP;   // L [P | Fu0 | Fu1] behind the V wait
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
   // <= PDG_THREAD_CAP threads per CTA: 384 keeps >= 168 registers per thread
   // (profiles/round1_compact_ops_ab.txt: compact operators + 384 beat 512)
@@ -688,7 +702,7 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
 #pragma unroll
       for (int jt = 0; jt < JTL; ++jt) lp[jt][0] = lp[jt][1] = 0.0;
 #pragma unroll
-      for (int s2 = 0; s2 < KS; ++s2) {
+      for (int s2 = 0; s2 < (C::LPL ? 0 : KS); ++s2) {
         const int k = kmap(s2, tig, KS, C::KP);
         const int fo = ((t * KS + s2) << 5) + lane;
 #if PDG_COMPACT_OPS
@@ -723,7 +737,8 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
         }
       }
       // G4: LY = LP Dt^T, A fragments of LP gathered within each lane quad
-      double ly[JT][2];
+      double ly[JT][2], lf0 = 0.0, lf1 = 0.0;
+      auto finish_lp = [&]() {
 #pragma unroll
       for (int jt = 0; jt < JT; ++jt) ly[jt][0] = ly[jt][1] = 0.0;
       if (vol) {
@@ -745,11 +760,13 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
         if (C::DOT0) d0 += __shfl_xor_sync(0xffffffffu, d0, 2);
         d1 += __shfl_xor_sync(0xffffffffu, d1, 2);
       }
-      const double lf0 = C::DOT0 ? d0 : __shfl_sync(0xffffffffu, lp[NQ / 8][c0 & 1], gid * 4 + c0 / 2);
+      lf0 = C::DOT0 ? d0 : __shfl_sync(0xffffffffu, lp[NQ / 8][c0 & 1], gid * 4 + c0 / 2);
       constexpr int cv = NQ - 8 * (JT - 1); // C::F1V: column of L Fu1 in the last L V tile
-      const double lf1 = C::FUV ? d1
-                         : C::F1V ? __shfl_sync(0xffffffffu, lv[JT - 1][cv & 1], gid * 4 + cv / 2)
-                                  : __shfl_sync(0xffffffffu, lp[(NQ + 1) / 8][c1 & 1], gid * 4 + c1 / 2);
+      lf1 = C::FUV ? d1
+            : C::F1V ? __shfl_sync(0xffffffffu, lv[JT - 1][cv & 1], gid * 4 + cv / 2)
+                     : __shfl_sync(0xffffffffu, lp[(NQ + 1) / 8][c1 & 1], gid * 4 + c1 / 2);
+      };
+      if (!C::LPL) finish_lp();
       // G5: quad-face lifts; the velocity lift of each face is kept separately
       // and scaled by that face's normal in the epilogue
       double qp[JT][2], qu[3][JT][2];
@@ -790,8 +807,13 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
 #endif
 #pragma unroll
           for (int jt = 0; jt < JT; ++jt) dmma(lv[jt], la, V[(8 * jt + gid) * VST + k]);
+          if (C::LPL) {
+#pragma unroll
+            for (int jt = 0; jt < JL; ++jt) dmma(lp[jt], la, src[jt][k]);
+          }
         }
       }
+      if (C::LPL) finish_lp();
       // epilogue: rows i, columns j = 8 jt + 2 tig + c; results straight to HBM
       const double tzJ = G[W_TZJ], jfb = G[W_JFB], jft = G[W_JFT];
       const double kappa = G[W_KAPPA], irho = G[W_IRHO];
