@@ -136,8 +136,10 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #ifndef PDG_MBAR_SYNC_N4
 #define PDG_MBAR_SYNC_N4 1
 #endif
+// N = 6 (end-of-element barrier kept, V exchange only) with PDG_MB_LP_LATE: -0.5%;
+// N = 7: +2.7%, so off (profiles/round2_mbar_ab.txt)
 #ifndef PDG_MBAR_SYNC_N6
-#define PDG_MBAR_SYNC_N6 0
+#define PDG_MBAR_SYNC_N6 1
 #endif
 #ifndef PDG_MBAR_SYNC_N7
 #define PDG_MBAR_SYNC_N7 0
