@@ -271,7 +271,8 @@ inline int ticket_batch(int N) {
   if (env > 0) return env;
   // measured sweeps, round 1 (profiles/round1_ticket_batch.txt; after the schedule
   // changes N = 4 prefers 4: profiles/round1_ticket_batch2.txt)
-  return N <= 3 ? 8 : (N == 4 ? 4 : 2);
+  // N = 7: one element per ticket, -0.8% after the round-2 schedule changes (profiles/round2_mbar_ab.txt)
+  return N <= 3 ? 8 : (N == 4 ? 4 : (N >= 7 ? 1 : 2));
 }
 
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
