@@ -73,12 +73,11 @@ __host__ __device__ constexpr bool tet_tables_global(int N) { return N >= PDG_TE
 #ifndef PDG_TET_LAUNDER
 #define PDG_TET_LAUNDER 1
 #endif
-// DMMA issue order of the volume products: 0 = gr gs gt dv dv dv, 1 = gr dv gs dv gt dv
-// (measured equal: DMMA latency is 26 cycles against a 16-cycle issue interval per
-// SM sub-partition, scripts/micro/dmma_latency.cu, so two chains already saturate)
-#ifndef PDG_TET_ORDER
-#define PDG_TET_ORDER 0
-#endif
+// (Measured and removed, profiles/round2_tet_ab.txt / round2_mbar_ab.txt: interleaving
+// the divergence chain with the gradient DMMAs -- equal, a dependent DMMA takes 26
+// cycles against a 16-cycle issue interval, scripts/micro/dmma_latency.cu; the gradient
+// products straight from the staged state before the fluxes -- +3..10%, registers;
+// publishing the next batch index late -- neutral.)
 
 // the next batch index in two slots alternating with the batch parity: a slot is
 // rewritten only after every thread has read it, so the barrier that protected
@@ -95,20 +94,6 @@ __host__ __device__ constexpr bool tet_tables_global(int N) { return N >= PDG_TE
 // -3.5 / -2.8 / -4.7% (slot parity alone: +0.2 / -0.6 / -0.1%)
 #ifndef PDG_TET_END_MBAR
 #define PDG_TET_END_MBAR 1
-#endif
-
-// gradient products D_a P straight from the staged state (no W columns needed)
-// between issuing the neighbour gathers and using them
-#ifndef PDG_TET_GRAD_FIRST
-#define PDG_TET_GRAD_FIRST 0
-#endif
-// (N = 5, 7 would spill with the gradient accumulators live across the flux phase)
-#define PDG_TET_GF(N) (PDG_TET_GRAD_FIRST && (N) != 5 && (N) != 7)
-
-// the next batch index published just before the flux barrier instead of right after
-// the ticket atomic, so the atomic's round trip overlaps the gathers and fluxes
-#ifndef PDG_TET_LATE_SLOT
-#define PDG_TET_LATE_SLOT 0
 #endif
 
 #ifndef PDG_TET_PAD_STATE
@@ -281,7 +266,7 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
     long long bn = 0;
     if (tt == 0) {
       bn = grab();
-      if (!(PDG_TET_LATE_SLOT && PDG_TET_SLOT_PARITY)) slot[PDG_TET_SLOT_PARITY ? 1 + (it & 1) : 1] = bn;
+      slot[PDG_TET_SLOT_PARITY ? 1 + (it & 1) : 1] = bn;
     }
     const double* U = stg0 + s * C::STAGE;
     const double* G = U + C::UB;
@@ -331,29 +316,13 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
         const double* Ut = U + t * C::US;
         const double* Gt = G + t * kTG;
         const double ux = Ut[NP + n], uy = Ut[2 * NP + n], uz = Ut[3 * NP + n];
-        if (!PDG_TET_GF(N)) BVb[t * VST + n] = Ut[n];
+        BVb[t * VST + n] = Ut[n];
         BVb[(kTB + t) * VST + n] = Gt[T_RX] * ux + Gt[T_RY] * uy + Gt[T_RZ] * uz;
         BVb[(2 * kTB + t) * VST + n] = Gt[T_SX] * ux + Gt[T_SY] * uy + Gt[T_SZ] * uz;
         BVb[(3 * kTB + t) * VST + n] = Gt[T_TX] * ux + Gt[T_TY] * uy + Gt[T_TZ] * uz;
       }
     }
     };
-    double gr[2] = {0.0, 0.0}, gs[2] = {0.0, 0.0}, gt[2] = {0.0, 0.0};
-    auto grad_products = [&]() {
-      if (vol) {
-#pragma unroll
-        for (int s2 = 0; s2 < KS; ++s2) {
-          const int fo = ((w * KS + s2) << 5) + lane;
-          const double ar = tab(sD, fo), as = tab(sD, C::DTAB + fo), at = tab(sD, 2 * C::DTAB + fo);
-          // B(k = node, n = tet gid) from the tet's state slot (zero A beyond NP)
-          const double bp = U[gid * C::US + 4 * s2 + tig];
-          dmma(gr, ar, bp);
-          dmma(gs, as, bp);
-          dmma(gt, at, bp);
-        }
-      }
-    };
-    if (PDG_TET_GF(N) && !surf) grad_products();
     // ---- fluxes of the batch (scaled by J_f / J) and the W_a columns ------------
     if (kBvFirst && !surf) {
       end_wait();
@@ -388,7 +357,6 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
           }
         }
       }
-      if (PDG_TET_GF(N)) grad_products(); // own state only, while the gathers are in flight
       end_wait();
       if (kBvFirst) build_bv(); // shared-memory work while the gathers are in flight
 #pragma unroll
@@ -425,11 +393,10 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
     end_wait();
     if (!kBvFirst) build_bv();
     if (PDG_TET_RES_LATE) load_res();
-    if (PDG_TET_LATE_SLOT && PDG_TET_SLOT_PARITY && tt == 0) slot[1 + (it & 1)] = bn; // read after the barrier
     team_sync(bar_id, 32 * T);
 
     // ---- row tile w: volume and lift products -------------------------------------
-    double dv[2] = {0.0, 0.0};
+    double gr[2] = {0.0, 0.0}, gs[2] = {0.0, 0.0}, gt[2] = {0.0, 0.0}, dv[2] = {0.0, 0.0};
     double lp[2] = {0.0, 0.0}, lu[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
     if (vol) {
 #pragma unroll
@@ -437,26 +404,13 @@ __global__ void __launch_bounds__(TDCfg<N, NST>::THREADS, 1) tet_dmma_kernel(con
         const int fo = ((w * KS + s2) << 5) + lane;
         const double ar = tab(sD, fo), as = tab(sD, C::DTAB + fo), at = tab(sD, 2 * C::DTAB + fo);
         const int bo = gid * VST + 4 * s2 + tig;
-        const double bp = PDG_TET_GF(N) ? 0.0 : BVb[bo];
-        if (PDG_TET_GF(N)) {
-          dmma(dv, ar, BVb[kTB * VST + bo]);
-          dmma(dv, as, BVb[2 * kTB * VST + bo]);
-          dmma(dv, at, BVb[3 * kTB * VST + bo]);
-        } else if (PDG_TET_ORDER == 1) {
-          dmma(gr, ar, bp);
-          dmma(dv, ar, BVb[kTB * VST + bo]);
-          dmma(gs, as, bp);
-          dmma(dv, as, BVb[2 * kTB * VST + bo]);
-          dmma(gt, at, bp);
-          dmma(dv, at, BVb[3 * kTB * VST + bo]);
-        } else {
-          dmma(gr, ar, bp);
-          dmma(gs, as, bp);
-          dmma(gt, at, bp);
-          dmma(dv, ar, BVb[kTB * VST + bo]);
-          dmma(dv, as, BVb[2 * kTB * VST + bo]);
-          dmma(dv, at, BVb[3 * kTB * VST + bo]);
-        }
+        const double bp = BVb[bo];
+        dmma(gr, ar, bp);
+        dmma(gs, as, bp);
+        dmma(gt, at, bp);
+        dmma(dv, ar, BVb[kTB * VST + bo]);
+        dmma(dv, as, BVb[2 * kTB * VST + bo]);
+        dmma(dv, at, BVb[3 * kTB * VST + bo]);
       }
     }
     if (surf) {

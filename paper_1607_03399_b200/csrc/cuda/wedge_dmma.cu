@@ -126,18 +126,19 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 
 // the two per-element team exchanges (fluxes -> products, V -> its lift) through
 // mbarriers instead of bar.sync: a warp arrives when its part is written and waits
-// only where it reads the others' part, so V-independent products (the lifts of
-// [P | Fu0 | Fu1], LY and the quad-face lifts) run between the V arrival and the
-// V wait, and (PDG_MB_VOL_AFTER, where the volume products are not issued first)
-// the element's volume products between the flux arrival and the flux wait.
-// Measured (profiles/round2_mbar_ab.txt): N = 5 -1.7% (adopted), N = 4 +0.4% alone and
-// -1.4% with PDG_MB_LP_LATE (adopted); volume products after the flux arrival +1.3% at
-// N = 5 (not adopted)
+// only where it reads the others' part.  With the volume products issued first, the
+// L [P | Fu0 | Fu1] product and L V run behind the V wait and share their L fragments
+// (PDG_MB_LP_LATE: one L read per element), and the quad-face lifts between the V
+// arrival and the V wait absorb the warps' skew.  The flux exchange goes through an
+// mbarrier where the parity flux buffers allow it (no end-of-element barrier, N <= 5).
+// Measured (profiles/round2_mbar_ab.txt): N = 5 -1.7% (exchanges) and -1.1% (shared L),
+// N = 4 -1.4% (both), N = 6 -0.5% (V exchange + shared L), N = 7 +2.7% (off).  Rejected
+// there and removed after measurement: volume products between the flux arrival and
+// wait, late ticket-slot publication, flux-lift dot products / Fu1 in the V padding
+// column at N = 6, 7, 16-byte normal loads.
 #ifndef PDG_MBAR_SYNC_N4
 #define PDG_MBAR_SYNC_N4 1
 #endif
-// N = 6 (end-of-element barrier kept, V exchange only) with PDG_MB_LP_LATE: -0.5%;
-// N = 7: +2.7%, so off (profiles/round2_mbar_ab.txt)
 #ifndef PDG_MBAR_SYNC_N6
 #define PDG_MBAR_SYNC_N6 1
 #endif
@@ -148,44 +149,8 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #define PDG_MBAR_SYNC(N) \
   ((N) == 5 || ((N) == 4 && PDG_MBAR_SYNC_N4) || ((N) == 6 && PDG_MBAR_SYNC_N6) || ((N) == 7 && PDG_MBAR_SYNC_N7))
 #endif
-// the grabber publishes the next element index at the flux exchange instead of right
-// after the ticket atomic (with the mbarrier exchanges after the flux wait, the V
-// exchange ordering it before every reader; with bar.sync just before the flux
-// barrier), so the atomic's round trip overlaps the gathers and the flux phase
-#ifndef PDG_MB_LATE_SLOT
-#define PDG_MB_LATE_SLOT 0
-#endif
-// with the mbarrier exchanges and the volume products issued first, the L [P | Fu0 | Fu1]
-// product moves behind the V wait too and shares its L fragments with L V (one
-// L read per element instead of two; only the quad-face lifts cover the V skew)
-// Measured (profiles/round2_mbar_ab.txt): N = 5 -1.1%; with it the mbarrier exchanges
-// pay at N = 4 too (-1.4% together)
 #ifndef PDG_MB_LP_LATE
 #define PDG_MB_LP_LATE 1
-#endif
-#ifndef PDG_MB_VOL_AFTER
-#define PDG_MB_VOL_AFTER 0
-#endif
-
-// at N = 6, 7 the last 8-column tile of the [P | Fu0 | Fu1] product holds only the
-// tri-face velocity fluxes (1 or 2 of 8 columns): those lifts are dot products on
-// the FP64 cores instead (the lane's A fragment times the flux at its k, reduced
-// over the lane quad), one DMMA per k-step less
-#ifndef PDG_FU_DOT
-#define PDG_FU_DOT 0
-#endif
-
-// N = 6: the [P | Fu0 | Fu1] product's second tile holds only Fu1; instead Fu1
-// rides in the free padding column NQ of the V operand, so L Fu1 comes out of the
-// L V product and the second tile's DMMAs go (KS per warp and element)
-#ifndef PDG_FU1_IN_V
-#define PDG_FU1_IN_V 0
-#endif
-
-// the epilogue's 15 face normals read as 16-byte pairs (8 shared loads per lane
-// instead of 15; the record is 16-byte aligned in the stage)
-#ifndef PDG_NRM_VEC
-#define PDG_NRM_VEC 0
 #endif
 
 /// k index of lane column tig in k-step s (see PDG_KPERM)
@@ -200,11 +165,6 @@ struct DCfg {
   static constexpr int IT = it_of(N), KS = ks_of(N), KT = kt_of(N);
   static constexpr int JT = ceil_div(NQ, 8), NPJ = 8 * JT;   // slice column tiles
   static constexpr int JTL = ceil_div(NQ + 2, 8);            // [P | Fu0 | Fu1] tiles
-  static constexpr bool FUV = PDG_FU_DOT && 8 * (JTL - 1) >= NQ; // last tile = fluxes only
-  // Fu1 alone in the last tile, and L V complete before the epilogue setup (no deferred L V)
-  static constexpr bool F1V = PDG_FU1_IN_V && !FUV && NQ + 1 == 8 * JT && !(PDG_MBAR_SYNC(N) && !PDG_SPLIT_ISSUE);
-  static constexpr int JL = (FUV || F1V) ? JTL - 1 : JTL;      // tiles on the tensor cores
-  static constexpr bool DOT0 = FUV && NQ >= 8 * (JTL - 1);     // Fu0 in the last tile too
   static constexpr int T = IT;                               // warps per team
   // per-wedge operator block sizes in HBM / the stage buffer
   static constexpr int LF = PDG_COMPACT_OPS ? lcomp_of(N) : lfrag_of(N);
@@ -248,8 +208,7 @@ struct DCfg {
   // measured (profiles/round1_volfirst_ab.txt): N = 4 -2.8%, N = 6 -4.5%, N = 7 -6.5%,
   // N = 5 +0.4% before the mbarrier exchanges, -0.6% with them (PDG_VF_N5)
   static constexpr bool VF = PDG_VOL_FIRST && (N != 5 || PDG_VF_N5);
-  static constexpr bool VA = MBF && !VF && PDG_MB_VOL_AFTER; // volume products after the flux arrival
-  static constexpr bool VP = VF || VA;                      // volume products outside G1 / G2
+  static constexpr bool VP = VF;                            // volume products outside G1 / G2
   static constexpr bool LPL = PDG_MB_LP_LATE && MB && VP;   // L [P | Fu0 | Fu1] behind the V wait
   static constexpr int TPB_SMEM = (SMEM_BUDGET / 8 - TABLES) / PER_TEAM;
   // <= PDG_THREAD_CAP threads per CTA: 384 keeps >= 168 registers per thread
@@ -524,8 +483,7 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
     long long en = 0;
     if (grabber) {
       en = grab();
-      if (!PDG_MB_LATE_SLOT || SPLIT)
-        slot[1 + (n & 1)] = en; // parity slots: rewritten only after every thread read it
+      slot[1 + (n & 1)] = en; // parity slots: rewritten only after every thread read it
     }
     const double* U = stg0 + s * C::STAGE;
     const double* R = U + C::USTR;
@@ -633,11 +591,8 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
     }
     if (C::MBF) {
       mbar_arrive(fbar);
-      if (C::VA) volume_products(); // own state only: covers the other warps' fluxes
       mbar_wait(fbar, n & 1);
-      if (PDG_MB_LATE_SLOT && grabber) slot[1 + (n & 1)] = en; // read after the V exchange
     } else {
-      if (PDG_MB_LATE_SLOT && !SPLIT && grabber) slot[1 + (n & 1)] = en; // read after the barrier
       team_sync(bar_id, 32 * T);
     }
     // every warp of the team has left the previous element: its stage may be refilled
@@ -680,7 +635,6 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
           if (i < NT && j < NQ) V[j * VST + i] = -d[c] + fb * sProf[j] + ftop * sProf[NQ + j];
         }
       }
-      if (C::F1V && tig == 0 && i < NT) V[NQ * VST + i] = surf ? Ftu[NT + i] : 0.0; // column NQ: Fu1
     }
     if (C::MB)
       mbar_arrive(vbar); // L V waits for it after the V-independent products
@@ -698,8 +652,7 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
         const int nc = 8 * jt + gid;
         src[jt] = nc < NQ ? Us + nc * SP : (nc == NQ ? Ftu : (nc == NQ + 1 ? Ftu + NT : Zero));
       }
-      constexpr int JL = C::JL;
-      double lv[JT][2], lp[JTL][2], d0 = 0.0, d1 = 0.0; // d0, d1: C::FUV dot products
+      double lv[JT][2], lp[JTL][2];
 #pragma unroll
       for (int jt = 0; jt < JT; ++jt) lv[jt][0] = lv[jt][1] = 0.0;
 #pragma unroll
@@ -719,14 +672,10 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
           cx = rx * dr + sxm * ds;
           cy = ry * dr + sym * ds;
         }
-        if (C::FUV && !PDG_MEMONLY) {
-          if (C::DOT0) d0 = fma(la, Ftu[k], d0);
-          d1 = fma(la, Ftu[NT + k], d1);
-        }
 #pragma unroll
         for (int jt = 0; jt < JTL; ++jt) {
-          const double bp = jt < JL ? src[jt][k] : 0.0;
-          if (!PDG_MEMONLY && jt < JL) dmma(lp[jt], la, bp);
+          const double bp = src[jt][k];
+          if (!PDG_MEMONLY) dmma(lp[jt], la, bp);
           if (jt < JT) {
             const int jb = 8 * jt + gid;
             if (vol && !C::VP) {
@@ -757,17 +706,8 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
       }
       // L fu_bottom, L fu_top of this row (columns NQ, NQ+1 of the G3 product)
       constexpr int c0 = NQ % 8, c1 = (NQ + 1) % 8;
-      if (C::FUV) { // sum the lane quad's partial dot products
-        if (C::DOT0) d0 += __shfl_xor_sync(0xffffffffu, d0, 1);
-        d1 += __shfl_xor_sync(0xffffffffu, d1, 1);
-        if (C::DOT0) d0 += __shfl_xor_sync(0xffffffffu, d0, 2);
-        d1 += __shfl_xor_sync(0xffffffffu, d1, 2);
-      }
-      lf0 = C::DOT0 ? d0 : __shfl_sync(0xffffffffu, lp[NQ / 8][c0 & 1], gid * 4 + c0 / 2);
-      constexpr int cv = NQ - 8 * (JT - 1); // C::F1V: column of L Fu1 in the last L V tile
-      lf1 = C::FUV ? d1
-            : C::F1V ? __shfl_sync(0xffffffffu, lv[JT - 1][cv & 1], gid * 4 + cv / 2)
-                     : __shfl_sync(0xffffffffu, lp[(NQ + 1) / 8][c1 & 1], gid * 4 + c1 / 2);
+      lf0 = __shfl_sync(0xffffffffu, lp[NQ / 8][c0 & 1], gid * 4 + c0 / 2);
+      lf1 = __shfl_sync(0xffffffffu, lp[(NQ + 1) / 8][c1 & 1], gid * 4 + c1 / 2);
       };
       if (!C::LPL) finish_lp();
       // G5: quad-face lifts; the velocity lift of each face is kept separately
@@ -812,7 +752,7 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
           for (int jt = 0; jt < JT; ++jt) dmma(lv[jt], la, V[(8 * jt + gid) * VST + k]);
           if (C::LPL) {
 #pragma unroll
-            for (int jt = 0; jt < JL; ++jt) dmma(lp[jt], la, src[jt][k]);
+            for (int jt = 0; jt < JTL; ++jt) dmma(lp[jt], la, src[jt][k]);
           }
         }
       }
@@ -822,24 +762,10 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
       const double kappa = G[W_KAPPA], irho = G[W_IRHO];
       const double pa = p.a, pb = p.b, pdt = p.dt;
       double n_[5][3];
-      if (PDG_NRM_VEC) {
-        constexpr int nb = w_nrm(N) & ~1, nv = (w_nrm(N) + 15 - nb + 1) / 2;
-        double2 pr[nv];
 #pragma unroll
-        for (int v = 0; v < nv; ++v) pr[v] = *reinterpret_cast<const double2*>(G + nb + 2 * v);
+      for (int f = 0; f < 5; ++f)
 #pragma unroll
-        for (int f = 0; f < 5; ++f)
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            const int o = w_nrm(N) + 3 * f + a - nb;
-            n_[f][a] = (o & 1) ? pr[o >> 1].y : pr[o >> 1].x;
-          }
-      } else {
-#pragma unroll
-        for (int f = 0; f < 5; ++f)
-#pragma unroll
-          for (int a = 0; a < 3; ++a) n_[f][a] = nrm[3 * f + a];
-      }
+        for (int a = 0; a < 3; ++a) n_[f][a] = nrm[3 * f + a];
       // per-lane base offset of position (i, j = 2 tig); (jt, c, field) add constants
       const int lane_off = 2 * tig * ST + i;
       const double* Ul = Us + 2 * tig * SP + i; // padded rows: (field*NQ + j)*SP + i

@@ -71,11 +71,8 @@ constexpr int kComboCapW = 2048; // ints of neighbour node maps kept in shared m
 #ifndef PDG_WADG_MB
 #define PDG_WADG_MB 1
 #endif
-// the flux exchange through an mbarrier too; where the volume products are not
-// issued first (N = 5, 6) they run between the flux arrival and the flux wait
-#ifndef PDG_WADG_MB_FLUX
-#define PDG_WADG_MB_FLUX 0
-#endif
+// (the flux exchange through an mbarrier too, with the volume products between its
+// arrival and wait at N = 5, 6, measured +0.9 / -0.5% and removed: round2_mbar_ab.txt)
 #ifndef PDG_WADG_NOEND_MAX_N
 #define PDG_WADG_NOEND_MAX_N 7
 #endif
@@ -125,7 +122,7 @@ struct WCfg {
   static constexpr int FBUF = (PDG_WADG_NO_END_BARRIER && !PAD && NST_ == 2 && N <= PDG_WADG_NOEND_MAX_N) ? 2 : 1;
   static constexpr int WORK = BS + FBUF * FBW + UPS;
   static constexpr int SMEM_BUDGET = 225 * 1024;
-  static constexpr int HDR = PDG_WADG_MB_FLUX ? 8 : 6; // mbarriers + schedule slots
+  static constexpr int HDR = 6; // 3 mbarriers + 3 schedule slots
   static constexpr int NSTAGE = (NST_ == 2 && (TABLES + HDR + 2 * STAGE + WORK) * 8 <= SMEM_BUDGET) ? 2 : 1;
   static constexpr int PER_TEAM = HDR + NSTAGE * STAGE + WORK;
   static constexpr bool NOEND = FBUF == 2 && NSTAGE == 2;
@@ -271,14 +268,11 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
   double* Upad = Fbase + C::FBUF * C::FBW; // padded state copy (C::PAD)
   constexpr int SP = C::SP;
   constexpr bool MB = PDG_WADG_MB && C::NOEND;
-  constexpr bool MF = MB && PDG_WADG_MB_FLUX;
   uint64_t* vbar = bar + 5; // MB: pre-lift buffer exchange
-  uint64_t* fbar = bar + 6; // MF: flux exchange
   if (tt == 0) {
     mbar_init(bar, 1);
     mbar_init(bar + 1, 1);
     if (MB) mbar_init(vbar, 32 * T);
-    if (MF) mbar_init(fbar, 32 * T);
     fence_barrier_init();
   }
   __syncthreads();
@@ -478,13 +472,7 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
     }
     if (C::VF && !surf) vol_products();
     for (int q = tt; q < NC; q += 32 * T) sIJ[q] = 1.0 / (j0 + jr * sQr[q] + js * sQs[q]);
-    if (MF) {
-      mbar_arrive(fbar);
-      if (!C::VF) vol_products(); // own state only: covers the other warps' fluxes
-      mbar_wait(fbar, n & 1);
-    } else {
-      team_sync(bar_id, 32 * T);
-    }
+    team_sync(bar_id, 32 * T);
     // every warp of the team has left the previous element: its stage may be refilled
     if (C::NOEND && tt == 0 && en < p.Kw_active) {
       fence_proxy_async_smem();
@@ -507,7 +495,7 @@ __global__ void __launch_bounds__(WCfg<N, NST, TG>::THREADS, 1) wedge_wadg_kerne
     };
     if (!MB) ltilde();
 
-    if (!C::VF && !MF) vol_products();
+    if (!C::VF) vol_products();
 
     // ---- D: quad faces (jf0 R0_e + jf1 R1_e) [Fp_e | Fu_e] -------------------
     double qp[JT][2], qu[3][JT][2];
