@@ -153,6 +153,14 @@ constexpr int kWedgeStages = PDG_WEDGE_STAGES; // per-team TMA pipeline depth (1
 #define PDG_MB_LP_LATE 1
 #endif
 
+// LSERK stage: the media factor folded into the stage's dt (pdt kappa, pdt / rho once
+// per element) instead of scaling every rhs value (4 FP64 multiplies per output less).
+// Measured (profiles/round2_mbar_ab.txt): N = 6 / 7 -0.6 / -0.7% (FP64-pipe throttled),
+// N = 5 +0.4%, so from N = 6 on
+#ifndef PDG_EPI_FOLD_MIN_N
+#define PDG_EPI_FOLD_MIN_N 6
+#endif
+
 /// k index of lane column tig in k-step s (see PDG_KPERM)
 __host__ __device__ constexpr int kmap(int s, int tig, int KS, bool perm) {
   return (perm && s < 4 * (KS / 4)) ? 16 * (s >> 2) + 4 * tig + (s & 3) : 4 * s + tig;
@@ -796,13 +804,16 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
               ruy += n_[0][1] * t0 + n_[1][1] * t1 + n_[2][1] * u2 + n_[3][1] * u3 + n_[4][1] * u4;
               ruz += n_[0][2] * t0 + n_[1][2] * t1 + n_[2][2] * u2 + n_[3][2] * u3 + n_[4][2] * u4;
             }
-            if (media) {
+            constexpr bool FOLD = N >= PDG_EPI_FOLD_MIN_N && !AB3;
+            const bool fold = FOLD && lserk;
+            if (media && !fold) {
               rp *= kappa;
               rux *= irho;
               ruy *= irho;
               ruz *= irho;
             }
             const double rv[4] = {rp, rux, ruy, ruz};
+            const double sk = media ? pdt * kappa : pdt, si = media ? pdt * irho : pdt; // fold: per-field dt
             constexpr int cst[2] = {0, ST};
             constexpr int csp[2] = {0, SP};
 #pragma unroll
@@ -815,7 +826,8 @@ __global__ void __launch_bounds__(DCfg<N, NST, AB3>::THREADS, 1) wedge_dmma_kern
                 __stcs(rhsl + o, rv[f]);
                 __stcs(uol + o, Ul[ou] + pdt * (23.0 * rv[f] - 16.0 * Rl[o] + 5.0 * F2l[o]));
               } else if (lserk) {
-                const double rr = first ? pdt * rv[f] : pa * Rl[o] + pdt * rv[f];
+                const double sc = fold ? (f == 0 ? sk : si) : pdt;
+                const double rr = first ? sc * rv[f] : pa * Rl[o] + sc * rv[f];
                 __stcs(resl + o, rr); // streaming stores: evict first
                 __stcs(uol + o, Ul[ou] + pb * rr);
               } else {
